@@ -1,0 +1,207 @@
+"""Multi-GPU product: paper Alg. 2 over torch.distributed (one process per GPU).
+
+The reference simulates N nodes with threads and queues (cluster.py:287-379):
+broadcast operands and bounds, compute O_k in `_block` slices, gather them,
+cut the intervals into N contiguous ranges of near-equal work
+(`partition_by_ops`, cluster.py:261-280), let every node compute its range,
+gather the disjoint results.  Here a "node" is a GPU rank:
+
+  1. every rank derives the same bounds (`select_grid`, deterministic);
+  2. rank r counts O_k for its `_block` of intervals on its GPU
+     (pgpu_count_below) and the counts are all-gathered;
+  3. `partition_by_ops` gives each rank a contiguous packed-exponent range
+     [S_l1, S_l2); the GPU forms only the products inside it;
+  4. the disjoint, already ordered slices are all-gathered into rank order
+     (NCCL over NVLink for device tensors; gloo in the CPU tests).  No
+     reduction: equal exponents never straddle a bound (split.py:5-9).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .core import SENTINEL, check_compatible, check_product_fits
+from .split import GridParams, select_grid
+
+
+@dataclass(frozen=True)
+class ClusterPlan:
+    n_nodes: int
+    ranges: tuple
+    op_counts: tuple
+
+    def loads(self) -> tuple:
+        return tuple(sum(self.op_counts[lo:hi]) for lo, hi in self.ranges)
+
+
+def partition_by_ops(op_counts, n_nodes: int) -> ClusterPlan:
+    """Greedy cumulative cut (reference cluster.py:261-280): range r ends at
+    the first prefix whose sum reaches (r+1)/N of the total; each range's load
+    exceeds total/N by at most max(op_counts)."""
+    if n_nodes < 1:
+        raise ValueError(f"need at least one node, got {n_nodes}")
+    counts = [int(x) for x in op_counts]
+    total = sum(counts)
+    cuts = [0]
+    run = 0
+    k = 0
+    for r in range(1, n_nodes):
+        while run * n_nodes < r * total:
+            run += counts[k]
+            k += 1
+        cuts.append(k)
+    cuts.append(len(counts))
+    return ClusterPlan(n_nodes, tuple(zip(cuts[:-1], cuts[1:])), tuple(counts))
+
+
+def block(n_items: int, n_nodes: int, rank: int) -> tuple:
+    """Rank's slice of the interval list for the O_k computation (cluster.py:283-284)."""
+    return rank * n_items // n_nodes, (rank + 1) * n_items // n_nodes
+
+
+def rank_range(bounds, plan: ClusterPlan, rank: int) -> tuple:
+    """Packed [lo, hi) of a rank's interval range."""
+    l1, l2 = plan.ranges[rank]
+    lo = bounds[l1] if l1 < len(bounds) else SENTINEL
+    hi = bounds[l2] if l2 < len(bounds) else SENTINEL
+    if l1 == l2:
+        lo = hi = bounds[l1]
+    if l1 == 0:
+        lo = 0
+    return lo, hi
+
+
+def _allgather_obj(obj, group):
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, obj, group=group)
+    return out
+
+
+def plan_for_ranks(a, b, l: int, world: int, rank: int, count_fn, group=None):
+    """Bounds + partition, with the O_k of each rank's block all-gathered."""
+    bounds = select_grid(a, b, GridParams(l)).bounds
+    n_int = len(bounds) - 1
+    lo_b, hi_b = block(n_int, world, rank)
+    if hi_b > lo_b:
+        cum = count_fn(a, b, bounds[lo_b:hi_b + 1])
+        mine = [int(cum[k + 1] - cum[k]) for k in range(hi_b - lo_b)]
+    else:
+        mine = []
+    if world > 1:
+        parts = _allgather_obj((lo_b, mine), group)
+    else:
+        parts = [(lo_b, mine)]
+    op_counts = [0] * n_int
+    for start, cnts in parts:
+        op_counts[start:start + len(cnts)] = cnts
+    return bounds, partition_by_ops(op_counts, world)
+
+
+def gather_slices(exps, coef, group=None, device=None):
+    """All-gather disjoint ordered slices (torch tensors) into rank order.
+
+    exps: (n,) int64 view of the u64 exponents; coef: (n, w) int64 view of the
+    coefficient words.  Returns the concatenation on every rank.
+    """
+    import torch
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    n = torch.tensor([exps.shape[0]], dtype=torch.int64, device=exps.device)
+    ns = [torch.zeros_like(n) for _ in range(world)]
+    dist.all_gather(ns, n, group=group)
+    counts = [int(x.item()) for x in ns]
+    m = max(counts) if counts else 0
+    w = coef.shape[1]
+    if m == 0:
+        return exps[:0], coef[:0]
+    pe = torch.zeros(m, dtype=torch.int64, device=exps.device)
+    pc = torch.zeros((m, w), dtype=torch.int64, device=exps.device)
+    pe[:exps.shape[0]] = exps
+    pc[:exps.shape[0]] = coef
+    ge = torch.empty(world * m, dtype=torch.int64, device=exps.device)
+    gc = torch.empty((world * m, w), dtype=torch.int64, device=exps.device)
+    dist.all_gather_into_tensor(ge, pe, group=group)
+    dist.all_gather_into_tensor(gc, pc, group=group)
+    es = [ge[r * m:r * m + counts[r]] for r in range(world)]
+    cs = [gc[r * m:r * m + counts[r]] for r in range(world)]
+    return torch.cat(es), torch.cat(cs)
+
+
+def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
+    """Distributed product; every rank returns the full Polynomial.
+
+    `local_fn(a, b, lo, hi) -> RawProduct` and `count_fn(a, b, bounds)` default
+    to the CUDA library (parmul.native_mul / count_below); the CPU tests inject
+    oracle versions to exercise the partition and gather logic over gloo.
+    """
+    import torch
+    import torch.distributed as dist
+    from . import parmul
+    if cfg is None:
+        cfg = parmul.MulConfig()
+    check_compatible(a, b)
+    cls = type(a)
+    if a.is_zero or b.is_zero:
+        return cls.zero(a.layout, a.ctype)
+    check_product_fits(a, b)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if count_fn is None:
+        def count_fn(x, y, bnd):
+            return parmul.count_below(x, y, bnd, device=cfg.device)
+    if local_fn is None:
+        def local_fn(x, y, lo, hi):
+            return parmul.native_mul(parmul.Operand.from_poly(x), parmul.Operand.from_poly(y),
+                                     x.layout, lo=lo, hi=hi, path=cfg.path,
+                                     float_ordered=cfg.float_ordered, device=cfg.device)
+    bounds, plan = plan_for_ranks(a, b, cfg.l, world, rank, count_fn, group)
+    lo, hi = rank_range(bounds, plan, rank)
+    if lo < hi:
+        raw = local_fn(a, b, lo, hi)
+    else:
+        raw = None
+    if world == 1:
+        if raw is None:
+            return cls.zero(a.layout, a.ctype)
+        return parmul.to_poly(cls, a.layout, a.ctype, raw)
+    backend = dist.get_backend(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if backend == "nccl" else torch.device("cpu")
+    # coefficient words: f64 bit patterns or u64 limbs; widths agree across ranks
+    if raw is None:
+        e = np.zeros(0, np.uint64)
+        wd = 1
+        cw = np.zeros((0, 1), np.uint64)
+        kind = None
+    else:
+        e = raw.exps
+        cw = raw.coef.view(np.uint64).reshape(raw.exps.shape[0], -1)
+        wd = cw.shape[1]
+        kind = (raw.kind, raw.nl)
+    kinds = _allgather_obj((kind, wd), group)
+    wd = max(k[1] for k in kinds)
+    kind = next((k[0] for k in kinds if k[0] is not None), None)
+    if cw.shape[1] < wd:  # sign-extend narrower limb sets
+        ext = np.empty((cw.shape[0], wd), np.uint64)
+        ext[:, :cw.shape[1]] = cw
+        sign = (cw[:, -1].view(np.int64) >> 63).view(np.uint64) if cw.shape[0] else np.zeros(0, np.uint64)
+        for k in range(cw.shape[1], wd):
+            ext[:, k] = sign
+        cw = ext
+    te = torch.from_numpy(e.view(np.int64).copy()).to(dev)
+    tc = torch.from_numpy(cw.view(np.int64).copy()).to(dev)
+    ge, gc = gather_slices(te, tc, group)
+    exps = ge.cpu().numpy().view(np.uint64)
+    words = gc.cpu().numpy().view(np.uint64)
+    if kind is None:
+        return cls.zero(a.layout, a.ctype)
+    nkind, nl = kind
+    if a.ctype is float:
+        coef = words.reshape(-1).view(np.float64)
+    else:
+        coef = words
+        nl = wd
+    raw_all = parmul.RawProduct(exps, coef, nkind, nl, 0, "", 0, 0, {})
+    return parmul.to_poly(cls, a.layout, a.ctype, raw_all)

@@ -1,0 +1,787 @@
+// polymul_b200.cu -- C ABI and host orchestration of the B200 sparse
+// polynomial multiplier (see include/polymul_b200.h).
+//
+// One call = one product, the reference `parmul.mul` (parmul.py:91-109):
+//   1. operand checks: compatible/zero handled by the Python mirror;
+//      exponent-field fit (check_product_fits, core.py:365-385) and the exact
+//      coefficient width are proven here from device statistics;
+//   2. compaction of packed exponents into short order-preserving keys;
+//   3. the [lo, hi) packed range (split= lower bound, cluster range) becomes a
+//      compact key range [KL, KH);
+//   4. either the dense path (dense_path.cuh: sumset bytemap, per-interval
+//      private accumulators) or the general sort path (sort_path.cuh);
+//   5. zero-sum compaction and hand-back of (exps, coeffs) in ascending order
+//      (concat, merge.py:164-173).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdarg>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/polymul_b200.h"
+#include "common.cuh"
+#include "dense_path.cuh"
+#include "prep.cuh"
+#include "scan.cuh"
+#include "sort_path.cuh"
+
+using namespace pgpu;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+struct Status {
+  int code = PGPU_OK;
+};
+
+#define CUDA_TRY(x)                                                                   \
+  do {                                                                                \
+    cudaError_t e_ = (x);                                                             \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(e_ == cudaErrorMemoryAllocation ? PGPU_ENOMEM : PGPU_ECUDA,          \
+                  "%s failed: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define TRY(x)                 \
+  do {                         \
+    int r_ = (x);              \
+    if (r_ != PGPU_OK) return r_; \
+  } while (0)
+
+#define LAUNCHED(k) (ctx.launches += (k))
+
+// Per-device state: library stream and a retained stream-ordered pool.
+struct DeviceState {
+  bool init = false;
+  cudaStream_t stream = nullptr;
+};
+std::mutex g_mu;
+DeviceState g_dev[64];
+
+int device_setup(int dev, cudaStream_t* st) {
+  CUDA_TRY(cudaSetDevice(dev));
+  std::lock_guard<std::mutex> lk(g_mu);
+  DeviceState& d = g_dev[dev & 63];
+  if (!d.init) {
+    CUDA_TRY(cudaStreamCreateWithFlags(&d.stream, cudaStreamNonBlocking));
+    cudaMemPool_t pool;
+    CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t thr = ~0ull;
+    CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    d.init = true;
+  }
+  *st = d.stream;
+  return PGPU_OK;
+}
+
+// Stream-ordered scratch; everything not handed to the caller is freed at scope exit.
+struct Arena {
+  cudaStream_t st;
+  std::vector<void*> ptrs;
+  explicit Arena(cudaStream_t s) : st(s) {}
+  ~Arena() {
+    for (void* p : ptrs) cudaFreeAsync(p, st);
+  }
+  template <typename T>
+  int alloc(T** p, size_t count) {
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(PGPU_ENOMEM, "device allocation of %zu bytes failed: %s", bytes,
+                  cudaGetErrorString(e));
+    }
+    ptrs.push_back((void*)*p);
+    return PGPU_OK;
+  }
+  void release(void* p) {  // ownership moves to the caller
+    ptrs.erase(std::remove(ptrs.begin(), ptrs.end(), p), ptrs.end());
+  }
+};
+
+struct Timer {
+  bool on = false;
+  cudaStream_t st;
+  int n = 0;
+  cudaEvent_t ev[PGPU_NPHASE + 1];
+  const char* names[PGPU_NPHASE];
+  float acc[PGPU_NPHASE] = {0};
+  void start(cudaStream_t s, bool enable) {
+    on = enable;
+    st = s;
+    if (!on) return;
+    for (int k = 0; k <= PGPU_NPHASE; ++k) cudaEventCreate(&ev[k]);
+    cudaEventRecord(ev[0], st);
+  }
+  // close phase k (phases may repeat across batches: times accumulate)
+  void mark(int k, const char* name) {
+    if (!on) return;
+    names[k] = name;
+    if (k + 1 > n) n = k + 1;
+    cudaEventRecord(ev[PGPU_NPHASE], st);
+    cudaEventSynchronize(ev[PGPU_NPHASE]);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, ev[0], ev[PGPU_NPHASE]);
+    acc[k] += ms;
+    std::swap(ev[0], ev[PGPU_NPHASE]);
+  }
+  void finish(pgpu_result* r) {
+    if (!on) return;
+    r->n_phase = n;
+    for (int k = 0; k < n; ++k) {
+      r->phase_ms[k] = acc[k];
+      r->phase_name[k] = names[k];
+    }
+    for (int k = 0; k <= PGPU_NPHASE; ++k) cudaEventDestroy(ev[k]);
+  }
+};
+
+struct Ctx {
+  cudaStream_t st;
+  Arena* ar;
+  Timer tm;
+  int64_t launches = 0;
+  int sms = 148;
+};
+
+inline int grid_for(int64_t n, int threads, int cap) {
+  int64_t g = (n + threads - 1) / threads;
+  if (g < 1) g = 1;
+  if (g > cap) g = cap;
+  return (int)g;
+}
+
+inline int bitlen64(uint64_t x) { return x ? 64 - __builtin_clzll(x) : 0; }
+
+// Everything the product needs once operands are on the device.
+struct Problem {
+  const uint64_t* aexp;
+  const uint64_t* bexp;
+  const void* acoef;
+  const void* bcoef;
+  uint32_t na, nb;
+  int ck;          // coefficient kind
+  int nl;          // integer result limbs (0 for f64)
+  int need_bits;   // proven bound on |coefficient| bits + sign
+  KeyPlan P;
+  bool k32;        // keys fit 32 bits
+  void* ak;        // compact keys (uint32_t* or uint64_t*)
+  void* bk;
+  uint64_t KL, KH; // compact key range
+};
+
+// A finished slice of the result (device buffers owned by the arena).
+struct Slice {
+  uint64_t* exps;
+  uint64_t* coef;  // limbs (f64 bit patterns when nl == 1 and ck == f64)
+  uint64_t n;
+};
+
+// ---------------------------------------------------------------------------
+// Row edges + exclusive offsets of a key range; returns the pair count.
+// ---------------------------------------------------------------------------
+template <typename KT>
+int range_rows(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint32_t** rlo,
+               uint32_t** rhi, uint64_t** off, uint64_t* pairs) {
+  TRY(ctx.ar->alloc(rlo, pb.na));
+  TRY(ctx.ar->alloc(rhi, pb.na));
+  TRY(ctx.ar->alloc(off, pb.na));
+  uint64_t* part;
+  TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
+  k_edges<KT><<<grid_for(pb.na, 256, 1 << 30), 256, 0, ctx.st>>>(
+      (const KT*)pb.ak, pb.na, (const KT*)pb.bk, pb.nb, KL, KH, *rlo, *rhi);
+  LAUNCHED(1);
+  int g;
+  LAUNCHED(device_scan<uint64_t>(pb.na, LenGen{*rlo, *rhi}, OffOut{*off}, part, &g, ctx.st));
+  CUDA_TRY(cudaMemcpyAsync(pairs, part + g, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  return PGPU_OK;
+}
+
+template <typename KT>
+int count_at(Ctx& ctx, const Problem& pb, const std::vector<uint64_t>& bounds,
+             std::vector<uint64_t>& cum) {
+  cum.assign(bounds.size(), 0);
+  if (bounds.empty()) return PGPU_OK;
+  uint64_t* db;
+  unsigned long long* dc;
+  TRY(ctx.ar->alloc(&db, bounds.size()));
+  TRY(ctx.ar->alloc(&dc, bounds.size()));
+  CUDA_TRY(cudaMemcpyAsync(db, bounds.data(), bounds.size() * 8, cudaMemcpyHostToDevice, ctx.st));
+  CUDA_TRY(cudaMemsetAsync(dc, 0, bounds.size() * 8, ctx.st));
+  for (size_t b0 = 0; b0 < bounds.size(); b0 += 65535) {
+    unsigned nbnd = (unsigned)std::min<size_t>(65535, bounds.size() - b0);
+    dim3 grid(grid_for(pb.na, 256, 64), nbnd);
+    k_count_multi<KT><<<grid, 256, 0, ctx.st>>>((const KT*)pb.ak, pb.na, (const KT*)pb.bk, pb.nb,
+                                                db + b0, dc + b0);
+    LAUNCHED(1);
+  }
+  CUDA_TRY(cudaMemcpyAsync(cum.data(), dc, bounds.size() * 8, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  return PGPU_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Sort path over one compact key range [KL, KH) holding `pairs` pairs.
+// ---------------------------------------------------------------------------
+template <typename KT>
+int radix_sort(Ctx& ctx, KT** keys, uint64_t** vals, KT* kalt, uint64_t* valt, uint64_t n,
+               int bits) {
+  if (n <= 1 || bits <= 0) return PGPU_OK;
+  int G = (int)std::min<uint64_t>((n + kRsTile - 1) / kRsTile, (uint64_t)ctx.sms * 4);
+  if (G < 1) G = 1;
+  uint64_t per = (n + G - 1) / G;
+  per = (per + kRsTile - 1) / kRsTile * kRsTile;
+  G = (int)((n + per - 1) / per);
+  uint32_t* counts;
+  TRY(ctx.ar->alloc(&counts, (size_t)kRsDigits * G));
+  KT* kin = *keys;
+  uint64_t* vin = *vals;
+  KT* kout = kalt;
+  uint64_t* vout = valt;
+  for (int shift = 0; shift < bits; shift += 8) {
+    k_rs_hist<KT><<<G, kRsThreads, 0, ctx.st>>>(kin, n, per, shift, G, counts);
+    k_rs_scan<<<1, 1024, 0, ctx.st>>>(counts, kRsDigits * G);
+    k_rs_scatter<KT><<<G, kRsThreads, 0, ctx.st>>>(kin, vin, kout, vout, n, per, shift, G, counts);
+    LAUNCHED(3);
+    std::swap(kin, kout);
+    std::swap(vin, vout);
+  }
+  *keys = kin;
+  *vals = vin;
+  return PGPU_OK;
+}
+
+template <typename KT>
+int sort_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t pairs, Slice* out) {
+  out->n = 0;
+  if (pairs == 0) return PGPU_OK;
+  uint32_t *rlo, *rhi;
+  uint64_t* off;
+  uint64_t chk;
+  TRY(range_rows<KT>(ctx, pb, KL, KH, &rlo, &rhi, &off, &chk));
+  if (chk != pairs) return fail(PGPU_ECUDA, "pair count mismatch %llu vs %llu",
+                                (unsigned long long)chk, (unsigned long long)pairs);
+  // local key width: keys are stored relative to KL
+  uint64_t kmax_local = (KH == ~0ull ? ((pb.P.kbits >= 64) ? ~0ull : ((1ull << pb.P.kbits) - 1))
+                                     : KH - 1) - KL;
+  int bits = bitlen64(kmax_local);
+  KT *keys, *kalt;
+  uint64_t *vals, *valt;
+  TRY(ctx.ar->alloc(&keys, pairs));
+  TRY(ctx.ar->alloc(&vals, pairs));
+  TRY(ctx.ar->alloc(&kalt, pairs));
+  TRY(ctx.ar->alloc(&valt, pairs));
+  k_gen<KT><<<grid_for((int64_t)pb.na * 32, 256, ctx.sms * 16), 256, 0, ctx.st>>>(
+      (const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, off, pb.na, KL, keys, vals);
+  LAUNCHED(1);
+  ctx.tm.mark(1, "gen");
+  TRY(radix_sort<KT>(ctx, &keys, &vals, kalt, valt, pairs, bits));
+  ctx.tm.mark(2, "sort");
+  // heads -> segment starts (reuse the spare buffer as starts)
+  uint32_t* starts;
+  TRY(ctx.ar->alloc(&starts, pairs + 1));
+  uint32_t* part;
+  TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
+  int g;
+  LAUNCHED(device_scan<uint32_t>(pairs, HeadGen<KT>{keys}, HeadOut{starts}, part, &g, ctx.st));
+  uint32_t nseg;
+  CUDA_TRY(cudaMemcpyAsync(&nseg, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  uint32_t pe = (uint32_t)pairs;
+  CUDA_TRY(cudaMemcpyAsync(starts + nseg, &pe, 4, cudaMemcpyHostToDevice, ctx.st));
+  int nl = pb.nl ? pb.nl : 1;
+  uint64_t *sexp, *scoef;
+  uint32_t* snz;
+  TRY(ctx.ar->alloc(&sexp, nseg));
+  TRY(ctx.ar->alloc(&scoef, (size_t)nseg * nl));
+  TRY(ctx.ar->alloc(&snz, nseg));
+  int gr = grid_for(nseg, 256, 1 << 30);
+  if (pb.ck == PGPU_F64) {
+    k_seg_reduce_f64<KT><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, (const double*)pb.acoef,
+                                                (const double*)pb.bcoef, KL, pb.P, sexp,
+                                                (double*)scoef, snz);
+  } else {
+#define SEGRED(NL_, CK_)                                                                   \
+  k_seg_reduce_int<KT, NL_, CK_><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, pb.acoef, \
+                                                         pb.bcoef, KL, pb.P, sexp, scoef, snz)
+    if (pb.ck == PGPU_I64) {
+      if (nl == 1) SEGRED(1, 1); else if (nl == 2) SEGRED(2, 1); else SEGRED(3, 1);
+    } else {
+      if (nl == 1) SEGRED(1, 2); else if (nl == 2) SEGRED(2, 2); else SEGRED(3, 2);
+    }
+#undef SEGRED
+  }
+  LAUNCHED(1);
+  ctx.tm.mark(3, "reduce");
+  // compaction of zero sums
+  uint64_t *cexp, *ccoef;
+  TRY(ctx.ar->alloc(&cexp, nseg));
+  TRY(ctx.ar->alloc(&ccoef, (size_t)nseg * nl));
+  LAUNCHED(device_scan<uint32_t>(nseg, FlagGen{snz}, CompactOut{sexp, scoef, nl, cexp, ccoef}, part,
+                                 &g, ctx.st));
+  uint32_t nnz;
+  CUDA_TRY(cudaMemcpyAsync(&nnz, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  ctx.tm.mark(4, "compact");
+  out->exps = cexp;
+  out->coef = ccoef;
+  out->n = nnz;
+  return PGPU_OK;
+}
+
+// Split [KL, KH) into ranges of at most `cap` pairs, in ascending key order.
+template <typename KT>
+int plan_batches(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t total,
+                 uint64_t cap, std::vector<std::pair<uint64_t, uint64_t>>& ranges,
+                 std::vector<uint64_t>& counts) {
+  ranges.clear();
+  counts.clear();
+  if (total <= cap) {
+    ranges.push_back({KL, KH});
+    counts.push_back(total);
+    return PGPU_OK;
+  }
+  // candidate bounds: sums on a 64x64 grid of the pair matrix
+  std::vector<uint64_t> ak(pb.na), bk(pb.nb);
+  if (pb.k32) {
+    std::vector<uint32_t> a32(pb.na), b32(pb.nb);
+    CUDA_TRY(cudaMemcpyAsync(a32.data(), pb.ak, 4ull * pb.na, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaMemcpyAsync(b32.data(), pb.bk, 4ull * pb.nb, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaStreamSynchronize(ctx.st));
+    for (uint32_t i = 0; i < pb.na; ++i) ak[i] = a32[i];
+    for (uint32_t j = 0; j < pb.nb; ++j) bk[j] = b32[j];
+  } else {
+    CUDA_TRY(cudaMemcpyAsync(ak.data(), pb.ak, 8ull * pb.na, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaMemcpyAsync(bk.data(), pb.bk, 8ull * pb.nb, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  }
+  std::vector<uint64_t> cand;
+  const int L = 64;
+  for (int r = 0; r <= L; ++r)
+    for (int c = 0; c <= L; ++c) {
+      uint64_t i = std::min<uint64_t>((uint64_t)r * pb.na / L, pb.na - 1);
+      uint64_t j = std::min<uint64_t>((uint64_t)c * pb.nb / L, pb.nb - 1);
+      uint64_t k = ak[i] + bk[j];
+      if (k > KL && k < KH) cand.push_back(k);
+    }
+  std::sort(cand.begin(), cand.end());
+  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
+  std::vector<uint64_t> cum;
+  TRY(count_at<KT>(ctx, pb, cand, cum));
+  uint64_t below_KL;
+  {
+    std::vector<uint64_t> c0, b0{KL};
+    TRY(count_at<KT>(ctx, pb, b0, c0));
+    below_KL = c0[0];
+  }
+  // bounds list with cumulative counts (relative to KL)
+  std::vector<uint64_t> bnd{KL}, cm{0};
+  for (size_t k = 0; k < cand.size(); ++k) {
+    bnd.push_back(cand[k]);
+    cm.push_back(cum[k] - below_KL);
+  }
+  bnd.push_back(KH);
+  cm.push_back(total);
+  // refine oversize gaps by bisection in key space
+  for (size_t k = 0; k + 1 < bnd.size();) {
+    uint64_t c = cm[k + 1] - cm[k];
+    uint64_t hiK = bnd[k + 1];
+    if (hiK == ~0ull) {
+      // bound the open top by the largest possible key + 1
+      hiK = ak[pb.na - 1] + bk[pb.nb - 1] + 1;
+    }
+    if (c > cap && hiK - bnd[k] > 1) {
+      uint64_t mid = bnd[k] + (hiK - bnd[k]) / 2;
+      std::vector<uint64_t> cc, bb{mid};
+      TRY(count_at<KT>(ctx, pb, bb, cc));
+      bnd.insert(bnd.begin() + k + 1, mid);
+      cm.insert(cm.begin() + k + 1, cc[0] - below_KL);
+      continue;
+    }
+    if (c > cap)
+      return fail(PGPU_EUNSUPPORTED, "a single key holds %llu pairs, more than the batch "
+                                     "capacity %llu", (unsigned long long)c,
+                  (unsigned long long)cap);
+    ++k;
+  }
+  // greedy packing
+  size_t k = 0;
+  while (k + 1 < bnd.size()) {
+    size_t e = k + 1;
+    while (e + 1 < bnd.size() && cm[e + 1] - cm[k] <= cap) ++e;
+    ranges.push_back({bnd[k], bnd[e]});
+    counts.push_back(cm[e] - cm[k]);
+    k = e;
+  }
+  return PGPU_OK;
+}
+
+template <typename KT>
+int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice>& slices) {
+  size_t freeb = 0, totb = 0;
+  CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
+  uint64_t bpp = 2 * (sizeof(KT) + 8) + 4 + 8;  // records x2, starts, slack
+  uint64_t cap = (uint64_t)(freeb * 0.80) / bpp;
+  if (cap > 0xfffffff0ull) cap = 0xfffffff0ull;  // 32-bit positions inside a batch
+  const char* env = getenv("PGPU_BATCH_CAP");
+  if (env) cap = std::min<uint64_t>(cap, strtoull(env, nullptr, 10));
+  std::vector<std::pair<uint64_t, uint64_t>> ranges;
+  std::vector<uint64_t> counts;
+  TRY(plan_batches<KT>(ctx, pb, pb.KL, pb.KH, total, cap, ranges, counts));
+  for (size_t r = 0; r < ranges.size(); ++r) {
+    Slice s;
+    TRY(sort_range<KT>(ctx, pb, ranges[r].first, ranges[r].second, counts[r], &s));
+    if (s.n) slices.push_back(s);
+  }
+  return PGPU_OK;
+}
+
+// Dense path driver (kernels in dense_path.cuh)
+#include "dense_driver.inc"
+
+// ---------------------------------------------------------------------------
+int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Problem& pb,
+                  const pgpu_options& o) {
+  // layout -> KeyPlan (packed part)
+  KeyPlan& P = pb.P;
+  memset(&P, 0, sizeof P);
+  P.nf = lay->nfields;
+  P.order = lay->order;
+  for (int f = 0; f < P.nf; ++f) {
+    P.shift[f] = lay->shift[f];
+    P.mask[f] = lay->width[f] >= 64 ? ~0ull : ((1ull << lay->width[f]) - 1);
+  }
+  OperandStats* dst;
+  TRY(ctx.ar->alloc(&dst, 1));
+  CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(OperandStats), ctx.st));
+  int ga = grid_for(pb.na, 256, ctx.sms * 4), gb = grid_for(pb.nb, 256, ctx.sms * 4);
+  if (o.coef_kind == PGPU_F64) {
+    k_stats<0><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0);
+    k_stats<0><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1);
+  } else if (o.coef_kind == PGPU_I64) {
+    k_stats<1><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0);
+    k_stats<1><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1);
+  } else {
+    k_stats<2><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0);
+    k_stats<2><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1);
+  }
+  LAUNCHED(2);
+  OperandStats hs;
+  CUDA_TRY(cudaMemcpyAsync(&hs, dst, sizeof hs, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  if (hs.unsorted[0] || hs.unsorted[1])
+    return fail(PGPU_EINVAL, "operand exponents are not strictly ascending packed words");
+  // exponent fit (core.py:365-385): field sums must stay within the caps
+  for (int f = 0; f < P.nf; ++f) {
+    int w = lay->width[f];
+    uint64_t cap = P.mask[f];
+    if (f == 0) cap -= 1;  // grlex degree ceiling / lex top-field ceiling reserved
+    uint64_t s = hs.fmax[0][f] + hs.fmax[1][f];
+    if (s > cap || s < hs.fmax[0][f]) {
+      return fail(PGPU_EEXPONENT, "product %s field %d can reach %llu, field range is 0..%llu",
+                  (P.order == 0 && f == 0) ? "total degree" : "exponent", f,
+                  (unsigned long long)s, (unsigned long long)cap);
+    }
+    (void)w;
+  }
+  // exact coefficient width: |c| <= min(na,nb) * max|a| * max|b|
+  pb.nl = 0;
+  if (o.coef_kind != PGPU_F64) {
+    int need = (int)hs.cbits[0] + (int)hs.cbits[1] + bitlen64(std::min(pb.na, pb.nb)) + 1;
+    pb.need_bits = need;
+    int nl = (need + 63) / 64;
+    if (nl < 1) nl = 1;
+    if (nl > 3)
+      return fail(PGPU_ECOEFF, "exact coefficients may need %d bits; the widest accumulator is 192",
+                  need);
+    if (o.acc_limbs) {
+      if (o.acc_limbs < nl)
+        return fail(PGPU_ECOEFF, "requested %d-limb accumulator but the bound needs %d bits",
+                    o.acc_limbs, need);
+      nl = std::min(o.acc_limbs, 3);
+    }
+    pb.nl = nl;
+  }
+  // key compaction plan
+  int pos = 0;
+  P.dropped = (P.order == 0) ? P.nf - 1 : -1;
+  for (int f = P.nf - 1; f >= 0; --f) {
+    uint64_t s = hs.fmax[0][f] + hs.fmax[1][f];
+    int cw = bitlen64(s);
+    P.keep[f] = (cw > 0 && f != P.dropped) ? 1 : 0;
+    P.cpos[f] = pos;
+    P.cmask[f] = cw >= 64 ? ~0ull : ((1ull << cw) - 1);
+    if (P.keep[f]) pos += cw;
+  }
+  P.kbits = pos;
+  pb.k32 = pos <= 32;
+  size_t ksz = pb.k32 ? 4 : 8;
+  TRY(ctx.ar->alloc((uint8_t**)&pb.ak, ksz * pb.na));
+  TRY(ctx.ar->alloc((uint8_t**)&pb.bk, ksz * pb.nb));
+  if (pb.k32) {
+    k_compact<uint32_t><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.na, P, (uint32_t*)pb.ak);
+    k_compact<uint32_t><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.nb, P, (uint32_t*)pb.bk);
+  } else {
+    k_compact<uint64_t><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.na, P, (uint64_t*)pb.ak);
+    k_compact<uint64_t><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.nb, P, (uint64_t*)pb.bk);
+  }
+  LAUNCHED(2);
+  // packed [lo, hi) -> compact [KL, KH)
+  pb.KL = 0;
+  pb.KH = ~0ull;
+  unsigned long long* dthr;
+  TRY(ctx.ar->alloc(&dthr, 2));
+  unsigned long long init[2] = {~0ull, ~0ull};
+  CUDA_TRY(cudaMemcpyAsync(dthr, init, 16, cudaMemcpyHostToDevice, ctx.st));
+  uint64_t S[2] = {o.lo, o.hi};
+  bool need[2] = {o.lo != 0, o.hi != ~0ull};
+  for (int s = 0; s < 2; ++s) {
+    if (!need[s]) continue;
+    int g = grid_for(pb.na, 256, 1 << 30);
+    if (pb.k32)
+      k_threshold<uint32_t><<<g, 256, 0, ctx.st>>>(pb.aexp, (const uint32_t*)pb.ak, pb.na, pb.bexp,
+                                                   (const uint32_t*)pb.bk, pb.nb, S[s], dthr + s);
+    else
+      k_threshold<uint64_t><<<g, 256, 0, ctx.st>>>(pb.aexp, (const uint64_t*)pb.ak, pb.na, pb.bexp,
+                                                   (const uint64_t*)pb.bk, pb.nb, S[s], dthr + s);
+    LAUNCHED(1);
+  }
+  unsigned long long thr[2];
+  CUDA_TRY(cudaMemcpyAsync(thr, dthr, 16, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  if (need[0]) pb.KL = thr[0];  // ~0 when no pair reaches lo: empty range
+  if (need[1]) pb.KH = thr[1];  // ~0 when every pair is below hi
+  return PGPU_OK;
+}
+
+int copy_in(Ctx& ctx, const pgpu_poly* p, size_t csz, const pgpu_options& o, const uint64_t** exps,
+            const void** coef) {
+  if (o.inputs_on_device) {
+    *exps = p->exps;
+    *coef = p->coeffs;
+    return PGPU_OK;
+  }
+  uint64_t* e;
+  uint8_t* c;
+  TRY(ctx.ar->alloc(&e, p->n));
+  TRY(ctx.ar->alloc(&c, p->n * csz));
+  CUDA_TRY(cudaMemcpyAsync(e, p->exps, p->n * 8, cudaMemcpyHostToDevice, ctx.st));
+  CUDA_TRY(cudaMemcpyAsync(c, p->coeffs, p->n * csz, cudaMemcpyHostToDevice, ctx.st));
+  *exps = e;
+  *coef = c;
+  return PGPU_OK;
+}
+
+int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
+             const pgpu_options* opt, pgpu_result* out) {
+  if (!a || !b || !lay || !out) return fail(PGPU_EINVAL, "null argument");
+  pgpu_options o;
+  if (opt) o = *opt; else pgpu_default_options(&o);
+  memset(out, 0, sizeof *out);
+  out->coef_kind = o.coef_kind == PGPU_F64 ? PGPU_F64 : PGPU_I64;
+  out->on_device = o.outputs_on_device;
+  if (lay->nfields < 1 || lay->nfields > PGPU_MAX_FIELDS)
+    return fail(PGPU_EINVAL, "layout needs 1..%d fields", PGPU_MAX_FIELDS);
+  if (o.coef_kind < 0 || o.coef_kind > 2) return fail(PGPU_EINVAL, "unknown coefficient kind");
+  if (a->n < 0 || b->n < 0 || a->n > 0xffffffffll || b->n > 0xffffffffll)
+    return fail(PGPU_EINVAL, "operand sizes must be in [0, 2^32)");
+  if (o.lo >= o.hi) return fail(PGPU_EINVAL, "empty exponent range");
+  if (a->n == 0 || b->n == 0) return PGPU_OK;  // Polynomial.zero (parmul.py:102-103)
+
+  cudaStream_t lib_st;
+  TRY(device_setup(o.device, &lib_st));
+  Ctx ctx;
+  ctx.st = o.stream ? (cudaStream_t)o.stream : lib_st;
+  CUDA_TRY(cudaDeviceGetAttribute(&ctx.sms, cudaDevAttrMultiProcessorCount, o.device));
+  Arena ar(ctx.st);
+  ctx.ar = &ar;
+  ctx.tm.start(ctx.st, o.timing != 0);
+
+  Problem pb;
+  memset(&pb, 0, sizeof pb);
+  pb.ck = o.coef_kind;
+  pb.na = (uint32_t)a->n;
+  pb.nb = (uint32_t)b->n;
+  size_t csz = o.coef_kind == PGPU_I128 ? 16 : 8;
+  TRY(copy_in(ctx, a, csz, o, &pb.aexp, &pb.acoef));
+  TRY(copy_in(ctx, b, csz, o, &pb.bexp, &pb.bcoef));
+  TRY(build_problem(ctx, lay, opt, pb, o));
+  out->key_bits = pb.P.kbits;
+  out->acc_limbs = pb.nl ? pb.nl : 1;
+
+  std::vector<Slice> slices;
+  if (pb.KL < pb.KH) {
+    // total pairs in range
+    uint64_t total = 0;
+    {
+      std::vector<uint64_t> bb{pb.KL}, cb;
+      if (pb.k32) TRY(count_at<uint32_t>(ctx, pb, bb, cb)); else TRY(count_at<uint64_t>(ctx, pb, bb, cb));
+      uint64_t below_lo = cb[0];
+      uint64_t below_hi = (uint64_t)pb.na * pb.nb;
+      if (pb.KH != ~0ull) {
+        std::vector<uint64_t> bh{pb.KH}, ch;
+        if (pb.k32) TRY(count_at<uint32_t>(ctx, pb, bh, ch)); else TRY(count_at<uint64_t>(ctx, pb, bh, ch));
+        below_hi = ch[0];
+      }
+      total = below_hi - below_lo;
+    }
+    out->pairs = (int64_t)total;
+    ctx.tm.mark(0, "prep");
+    int path = o.path;
+    if (o.float_ordered && o.coef_kind == PGPU_F64) path = PGPU_PATH_SORT;
+    int used = PGPU_PATH_SORT;
+    if (path != PGPU_PATH_SORT) {
+      int r = dense_try(ctx, pb, total, slices, path == PGPU_PATH_DENSE, &used);
+      if (r != PGPU_OK) return r;
+    }
+    if (used == PGPU_PATH_SORT) {
+      if (pb.k32) TRY(run_sort_path<uint32_t>(ctx, pb, total, slices));
+      else TRY(run_sort_path<uint64_t>(ctx, pb, total, slices));
+    }
+    out->path_used = used;
+  }
+
+  // assemble the result
+  int nl = pb.nl ? pb.nl : 1;
+  uint64_t n = 0;
+  for (auto& s : slices) n += s.n;
+  out->n = (int64_t)n;
+  out->acc_limbs = nl;
+  if (o.outputs_on_device) {
+    uint64_t *e, *c;
+    if (slices.size() == 1) {
+      e = slices[0].exps;
+      c = slices[0].coef;
+    } else {
+      TRY(ar.alloc(&e, n));
+      TRY(ar.alloc(&c, n * nl));
+      uint64_t at = 0;
+      for (auto& s : slices) {
+        CUDA_TRY(cudaMemcpyAsync(e + at, s.exps, s.n * 8, cudaMemcpyDeviceToDevice, ctx.st));
+        CUDA_TRY(cudaMemcpyAsync(c + at * nl, s.coef, s.n * 8 * nl, cudaMemcpyDeviceToDevice, ctx.st));
+        at += s.n;
+      }
+    }
+    ar.release(e);
+    ar.release(c);
+    out->exps = e;
+    out->coeffs = c;
+  } else {
+    out->exps = (uint64_t*)malloc(std::max<uint64_t>(n, 1) * 8);
+    out->coeffs = malloc(std::max<uint64_t>(n, 1) * 8 * nl);
+    if (!out->exps || !out->coeffs) return fail(PGPU_ENOMEM, "host allocation failed");
+    uint64_t at = 0;
+    for (auto& s : slices) {
+      CUDA_TRY(cudaMemcpyAsync(out->exps + at, s.exps, s.n * 8, cudaMemcpyDeviceToHost, ctx.st));
+      CUDA_TRY(cudaMemcpyAsync((uint64_t*)out->coeffs + at * nl, s.coef, s.n * 8 * nl,
+                               cudaMemcpyDeviceToHost, ctx.st));
+      at += s.n;
+    }
+  }
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  ctx.tm.mark(5, "output");
+  ctx.tm.finish(out);
+  CUDA_TRY(cudaGetLastError());
+  out->kernel_launches = ctx.launches;
+  return PGPU_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+void pgpu_default_options(pgpu_options* o) {
+  memset(o, 0, sizeof *o);
+  o->coef_kind = PGPU_F64;
+  o->hi = ~0ull;
+}
+
+int pgpu_mul(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
+             const pgpu_options* opt, pgpu_result* out) {
+  int r = mul_impl(a, b, lay, opt, out);
+  if (r != PGPU_OK && out) {
+    // release anything already handed to the result
+    pgpu_free_result(out);
+  }
+  return r;
+}
+
+int pgpu_count_below(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
+                     const uint64_t* bounds, int64_t nbounds, const pgpu_options* opt,
+                     uint64_t* cum) {
+  if (!a || !b || !lay || !cum || (nbounds > 0 && !bounds)) return fail(PGPU_EINVAL, "null argument");
+  pgpu_options o;
+  if (opt) o = *opt; else pgpu_default_options(&o);
+  if (nbounds <= 0) return PGPU_OK;
+  if (a->n == 0 || b->n == 0) {
+    for (int64_t k = 0; k < nbounds; ++k) cum[k] = 0;
+    return PGPU_OK;
+  }
+  cudaStream_t lib_st;
+  TRY(device_setup(o.device, &lib_st));
+  Ctx ctx;
+  ctx.st = o.stream ? (cudaStream_t)o.stream : lib_st;
+  Arena ar(ctx.st);
+  ctx.ar = &ar;
+  Problem pb;
+  memset(&pb, 0, sizeof pb);
+  pb.na = (uint32_t)a->n;
+  pb.nb = (uint32_t)b->n;
+  size_t csz = o.coef_kind == PGPU_I128 ? 16 : 8;
+  o.coef_kind = o.coef_kind;
+  TRY(copy_in(ctx, a, csz, o, &pb.aexp, &pb.acoef));
+  TRY(copy_in(ctx, b, csz, o, &pb.bexp, &pb.bcoef));
+  // packed-space counting: the packed words themselves are the keys
+  pb.ak = (void*)pb.aexp;
+  pb.bk = (void*)pb.bexp;
+  std::vector<uint64_t> bv(bounds, bounds + nbounds), cv;
+  TRY(count_at<uint64_t>(ctx, pb, bv, cv));
+  for (int64_t k = 0; k < nbounds; ++k) cum[k] = cv[k];
+  return PGPU_OK;
+}
+
+void pgpu_free_result(pgpu_result* r) {
+  if (!r) return;
+  if (r->on_device) {
+    if (r->exps) cudaFree(r->exps);
+    if (r->coeffs) cudaFree(r->coeffs);
+  } else {
+    free(r->exps);
+    free(r->coeffs);
+  }
+  r->exps = nullptr;
+  r->coeffs = nullptr;
+  r->n = 0;
+}
+
+const char* pgpu_last_error(void) { return g_err.c_str(); }
+
+int pgpu_device_count(void) {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
+}
+
+int pgpu_abi_version(void) { return PGPU_ABI_VERSION; }
+
+}  // extern "C"

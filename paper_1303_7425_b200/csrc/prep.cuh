@@ -1,0 +1,142 @@
+// prep.cuh -- operand statistics, key compaction, range thresholds, row edges
+// and pair counting.
+//
+//   k_stats        per-field maxima (check_product_fits, core.py:365-385) and
+//                  coefficient magnitudes (accumulator-width proof)
+//   k_compact      packed word -> order-preserving short key (KeyPlan)
+//   k_threshold    packed bound S -> smallest compact key of a realisable sum
+//                  >= S (so split=/cluster ranges translate exactly)
+//   k_edges        per-row column range of a key interval (find_edge,
+//                  split.py:131-166, computed by binary search per row)
+//   k_count_multi  cum[k] = #pairs below bounds[k] (count_ops, split.py:169-175)
+#pragma once
+#include "common.cuh"
+
+namespace pgpu {
+
+struct OperandStats {
+  unsigned long long fmax[2][kMaxFields];
+  unsigned int cbits[2];
+  unsigned int unsorted[2];
+};
+
+__device__ __forceinline__ int bitlen_u64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
+
+template <int CK>
+__global__ void __launch_bounds__(256)
+k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_t n, KeyPlan P,
+        OperandStats* st, int side) {
+  const int nf = P.nf;
+  __shared__ unsigned long long smax[kMaxFields];
+  __shared__ unsigned int sbits, sunsorted;
+  if (threadIdx.x < kMaxFields) smax[threadIdx.x] = 0;
+  if (threadIdx.x == 0) { sbits = 0; sunsorted = 0; }
+  __syncthreads();
+  unsigned long long lmax[kMaxFields];
+#pragma unroll
+  for (int f = 0; f < kMaxFields; ++f) lmax[f] = 0;
+  unsigned int lbits = 0, lbad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t e = exps[i];
+    if (i > 0 && exps[i - 1] >= e) lbad = 1;
+    if (e == ~0ull) lbad = 1;
+#pragma unroll
+    for (int f = 0; f < kMaxFields; ++f)
+      if (f < nf) {
+        unsigned long long v = (e >> P.shift[f]) & P.mask[f];
+        lmax[f] = v > lmax[f] ? v : lmax[f];
+      }
+    if constexpr (CK == 1) {
+      int64_t c = reinterpret_cast<const int64_t*>(coef)[i];
+      uint64_t mag = c < 0 ? (uint64_t)(-(c + 1)) + 1 : (uint64_t)c;
+      int b = bitlen_u64(mag);
+      lbits = b > (int)lbits ? b : lbits;
+    } else if constexpr (CK == 2) {
+      const uint64_t* p = reinterpret_cast<const uint64_t*>(coef) + 2 * i;
+      uint64_t lo = p[0], hi = p[1];
+      if ((int64_t)hi < 0) {  // magnitude of a negative 128-bit value
+        lo = ~lo; hi = ~hi;
+        lo += 1;
+        if (lo == 0) hi += 1;
+      }
+      int b = hi ? 64 + bitlen_u64(hi) : bitlen_u64(lo);
+      lbits = b > (int)lbits ? b : lbits;
+    }
+  }
+#pragma unroll
+  for (int f = 0; f < kMaxFields; ++f)
+    if (f < nf && lmax[f]) atomicMax(&smax[f], lmax[f]);
+  if (lbits) atomicMax(&sbits, lbits);
+  if (lbad) sunsorted = 1;
+  __syncthreads();
+  if (threadIdx.x < nf && smax[threadIdx.x]) atomicMax(&st->fmax[side][threadIdx.x], smax[threadIdx.x]);
+  if (threadIdx.x == 0) {
+    if (sbits) atomicMax(&st->cbits[side], sbits);
+    if (sunsorted) st->unsorted[side] = 1;
+  }
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_compact(const uint64_t* __restrict__ exps, int64_t n, KeyPlan P, KT* __restrict__ out) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = (KT)compact_word(exps[i], P);
+}
+
+// Smallest compact key of a pair whose packed sum is >= S (ULLONG_MAX if none).
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_threshold(const uint64_t* __restrict__ aexp, const KT* __restrict__ ak, uint32_t na,
+            const uint64_t* __restrict__ bexp, const KT* __restrict__ bk, uint32_t nb, uint64_t S,
+            unsigned long long* out) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long best = ~0ull;
+  if (i < na) {
+    uint32_t j = count_below<uint64_t>(bexp, nb, aexp[i], S);
+    if (j < nb) best = (unsigned long long)ak[i] + (unsigned long long)bk[j];
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    unsigned long long o = __shfl_xor_sync(0xffffffffu, best, d);
+    best = o < best ? o : best;
+  }
+  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(out, best);
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_edges(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk, uint32_t nb,
+        uint64_t KL, uint64_t KH, uint32_t* __restrict__ rlo, uint32_t* __restrict__ rhi) {
+  uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= na) return;
+  uint64_t ai = ak[i];
+  rlo[i] = count_below(bk, nb, ai, KL);
+  rhi[i] = count_below(bk, nb, ai, KH);
+}
+
+// cum[k] += #{(i,j): ak[i]+bk[j] < bounds[k]}; grid.y indexes bounds.
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_count_multi(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk, uint32_t nb,
+              const uint64_t* __restrict__ bounds, unsigned long long* cum) {
+  uint64_t K = bounds[blockIdx.y];
+  unsigned long long c = 0;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < na; i += gridDim.x * blockDim.x)
+    c += count_below(bk, nb, (uint64_t)ak[i], K);
+  c = warp_sum(c);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cum + blockIdx.y, c);
+}
+
+struct LenGen {
+  const uint32_t* lo;
+  const uint32_t* hi;
+  __device__ uint64_t operator()(uint64_t i) const { return (uint64_t)(hi[i] - lo[i]); }
+};
+
+struct OffOut {
+  uint64_t* off;
+  __device__ void operator()(uint64_t i, uint64_t ex, uint64_t) const { off[i] = ex; }
+};
+
+}  // namespace pgpu

@@ -1,0 +1,86 @@
+// scan.cuh -- device-wide exclusive scan over a generated sequence.
+//
+// Reduce-then-scan over G contiguous block ranges: pass 1 sums each range,
+// a single block scans the G partial sums, pass 2 rescans each range with its
+// carry-in and hands (index, exclusive prefix, value) to an output functor.
+// Used for row offsets, run-length heads, and zero-coefficient compaction.
+#pragma once
+#include "common.cuh"
+
+namespace pgpu {
+
+constexpr int kScanThreads = 256;
+
+template <typename T, typename Gen>
+__global__ void __launch_bounds__(kScanThreads)
+k_range_reduce(uint64_t n, uint64_t per, Gen gen, T* part) {
+  __shared__ T sh[33];
+  uint64_t beg = (uint64_t)blockIdx.x * per;
+  uint64_t end = beg + per < n ? beg + per : n;
+  T s = 0;
+  for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) s += gen(i);
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    T v = threadIdx.x < (blockDim.x >> 5) ? sh[threadIdx.x] : T(0);
+    v = warp_sum(v);
+    if (threadIdx.x == 0) part[blockIdx.x] = v;
+  }
+}
+
+// Exclusive scan of part[0..g) in place; part[g] = total.
+template <typename T>
+__global__ void __launch_bounds__(1024) k_part_scan(T* part, int g) {
+  __shared__ T sh[33];
+  T carry = 0;
+  for (int base = 0; base < g; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    T v = i < g ? part[i] : T(0);
+    T tot;
+    T ex = block_excl_scan(v, sh, &tot);
+    if (i < g) part[i] = carry + ex;
+    carry += tot;
+  }
+  if (threadIdx.x == 0) part[g] = carry;
+}
+
+template <typename T, typename Gen, typename Out>
+__global__ void __launch_bounds__(kScanThreads)
+k_range_scan(uint64_t n, uint64_t per, Gen gen, Out out, const T* part) {
+  __shared__ T sh[33];
+  uint64_t beg = (uint64_t)blockIdx.x * per;
+  uint64_t end = beg + per < n ? beg + per : n;
+  T carry = part[blockIdx.x];
+  for (uint64_t base = beg; base < end; base += blockDim.x) {
+    uint64_t i = base + threadIdx.x;
+    T v = i < end ? gen(i) : T(0);
+    T tot;
+    T ex = block_excl_scan(v, sh, &tot);
+    if (i < end) out(i, carry + ex, v);
+    carry += tot;
+  }
+}
+
+// Host driver.  `part` must hold >= G+1 elements (G <= kMaxScanBlocks).
+// Returns the number of kernel launches (3).  The total lands in part[G].
+constexpr int kMaxScanBlocks = 2048;
+
+template <typename T, typename Gen, typename Out>
+int device_scan(uint64_t n, Gen gen, Out out, T* part, int* g_out, cudaStream_t st) {
+  int g = (int)((n + 65535) / 65536);
+  if (g < 1) g = 1;
+  if (g > kMaxScanBlocks) g = kMaxScanBlocks;
+  uint64_t per = (n + g - 1) / g;
+  per = (per + kScanThreads - 1) / kScanThreads * kScanThreads;
+  if (per == 0) per = kScanThreads;
+  g = (int)((n + per - 1) / per);
+  if (g < 1) g = 1;
+  k_range_reduce<T><<<g, kScanThreads, 0, st>>>(n, per, gen, part);
+  k_part_scan<T><<<1, 1024, 0, st>>>(part, g);
+  k_range_scan<T><<<g, kScanThreads, 0, st>>>(n, per, gen, out, part);
+  *g_out = g;
+  return 3;
+}
+
+}  // namespace pgpu

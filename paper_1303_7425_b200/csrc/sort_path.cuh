@@ -1,0 +1,277 @@
+// sort_path.cuh -- the general "expand / sort / run-length reduce" pipeline.
+//
+// This is the north star's materialise-sort-reduce design and the path taken
+// for any input (wide keys, sparse products, the bit-exact float mode):
+//
+//   K1 k_gen        every pair (i, j) of a key range -> (compact key, i<<32|j)
+//                   (replaces the (a_i+b_j, i, j) creation of merge.py:41-60)
+//   K2 radix sort   stable LSD, 8-bit digits, on the significant key bits only
+//                   (replaces heapq ordering, merge.py:42-62; stability keeps
+//                   equal keys in increasing i, the reference's tie order)
+//   K3 heads/scan   run-length heads where the key changes -> segment starts
+//                   (replaces equal-exponent combining, merge.py:54-62)
+//   K4 seg reduce   one thread owns one output term and folds its segment in
+//                   order (acc = p_first; acc += p ...), merge.py:49-58
+//   K5 nz compact   drop zero sums (merge.py:63)
+#pragma once
+#include "common.cuh"
+#include "scan.cuh"
+
+namespace pgpu {
+
+// ---- K1: pair generation ---------------------------------------------------
+// One warp per row, lanes over consecutive columns: coalesced key loads and
+// coalesced record stores.  Row i's pairs land at off[i] in increasing j, rows
+// in increasing i, so the generation order is the reference's (i, j) order.
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_gen(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
+      const uint32_t* __restrict__ rhi, const uint64_t* __restrict__ off, uint32_t na,
+      uint64_t KL, KT* __restrict__ keys, uint64_t* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nwarps) {
+    uint32_t j0 = rlo[i], j1 = rhi[i];
+    if (j0 >= j1) continue;
+    uint64_t base = off[i] - j0;
+    uint64_t ai = (uint64_t)ak[i] - KL;  // wraps for rows below KL; the sum does not
+    for (uint32_t j = j0 + lane; j < j1; j += 32) {
+      keys[base + j] = (KT)(ai + (uint64_t)__ldg(bk + j));
+      vals[base + j] = ((uint64_t)i << 32) | j;
+    }
+  }
+}
+
+// ---- K2: LSD radix sort ----------------------------------------------------
+constexpr int kRsThreads = 256;
+constexpr int kRsWarps = kRsThreads / 32;
+constexpr int kRsIpt = 8;                          // items per thread per tile
+constexpr int kRsTile = kRsThreads * kRsIpt;       // 2048
+constexpr int kRsDigits = 256;
+
+__device__ __forceinline__ unsigned lanemask_lt() {
+  unsigned m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+// Lanes holding the same 8-bit digit (restricted to `valid` lanes).
+__device__ __forceinline__ unsigned digit_peers(unsigned d, unsigned valid) {
+  unsigned peers = valid;
+#pragma unroll
+  for (int b = 0; b < 8; ++b) {
+    unsigned bit = (d >> b) & 1u;
+    unsigned bal = __ballot_sync(0xffffffffu, bit);
+    peers &= bit ? bal : ~bal;
+  }
+  return peers;
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kRsThreads)
+k_rs_hist(const KT* __restrict__ keys, uint64_t n, uint64_t per, int shift, int G,
+          uint32_t* __restrict__ counts) {
+  __shared__ uint32_t wh[kRsWarps][kRsDigits];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wh[0][0])[k] = 0;
+  __syncthreads();
+  uint64_t beg = (uint64_t)blockIdx.x * per;
+  uint64_t end = beg + per < n ? beg + per : n;
+  for (uint64_t base = beg; base < end; base += kRsThreads) {
+    uint64_t idx = base + threadIdx.x;
+    bool ok = idx < end;
+    unsigned d = ok ? (unsigned)((uint64_t)keys[idx] >> shift) & 0xffu : 0u;
+    unsigned valid = __ballot_sync(0xffffffffu, ok);
+    unsigned peers = digit_peers(d, valid);
+    if (ok && (peers & lanemask_lt()) == 0) wh[w][d] += __popc(peers);
+    __syncwarp();
+  }
+  __syncthreads();
+  for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x) {
+    uint32_t s = 0;
+#pragma unroll
+    for (int q = 0; q < kRsWarps; ++q) s += wh[q][d];
+    counts[(uint64_t)d * G + blockIdx.x] = s;
+  }
+}
+
+// Exclusive scan of counts[256*G] in (digit, block) order, in place.
+__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* counts, int total) {
+  __shared__ uint32_t sh[33];
+  uint32_t carry = 0;
+  for (int base = 0; base < total; base += blockDim.x) {
+    int i = base + threadIdx.x;
+    uint32_t v = i < total ? counts[i] : 0u;
+    uint32_t tot;
+    uint32_t ex = block_excl_scan(v, sh, &tot);
+    if (i < total) counts[i] = carry + ex;
+    carry += tot;
+  }
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(kRsThreads)
+k_rs_scatter(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* __restrict__ kout,
+             uint64_t* __restrict__ vout, uint64_t n, uint64_t per, int shift, int G,
+             const uint32_t* __restrict__ offs) {
+  __shared__ uint32_t wcnt[kRsWarps][kRsDigits];
+  __shared__ uint32_t run_off[kRsDigits];
+  __shared__ uint32_t tstart[kRsDigits];
+  __shared__ uint32_t ttot[kRsDigits];
+  __shared__ uint32_t shs[33];
+  __shared__ KT skey[kRsTile];
+  __shared__ uint64_t sval[kRsTile];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x)
+    run_off[d] = offs[(uint64_t)d * G + blockIdx.x];
+  uint64_t beg = (uint64_t)blockIdx.x * per;
+  uint64_t end = beg + per < n ? beg + per : n;
+  for (uint64_t t0 = beg; t0 < end; t0 += kRsTile) {
+    for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wcnt[0][0])[k] = 0;
+    __syncthreads();
+    KT key[kRsIpt];
+    uint64_t val[kRsIpt];
+    uint32_t rank[kRsIpt];
+    unsigned dig[kRsIpt];
+    // warp w owns tile items [w*256, (w+1)*256): warp-major order is input order
+#pragma unroll
+    for (int k = 0; k < kRsIpt; ++k) {
+      uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
+      bool ok = idx < end;
+      key[k] = ok ? kin[idx] : KT(0);
+      val[k] = ok ? vin[idx] : 0ull;
+      dig[k] = ok ? (unsigned)((uint64_t)key[k] >> shift) & 0xffu : 0u;
+      unsigned valid = __ballot_sync(0xffffffffu, ok);
+      unsigned peers = digit_peers(dig[k], valid);
+      uint32_t c = ok ? wcnt[w][dig[k]] : 0u;
+      __syncwarp();
+      rank[k] = c + __popc(peers & lt);
+      if (ok && (peers & lt) == 0) wcnt[w][dig[k]] = c + __popc(peers);
+      __syncwarp();
+      if (!ok) dig[k] = 0xffffffffu;
+    }
+    __syncthreads();
+    // per digit: exclusive over warps, tile totals
+    for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x) {
+      uint32_t s = 0;
+#pragma unroll
+      for (int q = 0; q < kRsWarps; ++q) {
+        uint32_t c = wcnt[q][d];
+        wcnt[q][d] = s;
+        s += c;
+      }
+      ttot[d] = s;
+    }
+    __syncthreads();
+    {
+      uint32_t v = threadIdx.x < kRsDigits ? ttot[threadIdx.x] : 0u;
+      uint32_t tot;
+      uint32_t ex = block_excl_scan(v, shs, &tot);
+      if (threadIdx.x < kRsDigits) tstart[threadIdx.x] = ex;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRsIpt; ++k) {
+      if (dig[k] != 0xffffffffu) {
+        uint32_t pos = tstart[dig[k]] + wcnt[w][dig[k]] + rank[k];
+        skey[pos] = key[k];
+        sval[pos] = val[k];
+      }
+    }
+    __syncthreads();
+    uint32_t tn = (uint32_t)((end - t0) < (uint64_t)kRsTile ? (end - t0) : (uint64_t)kRsTile);
+    for (uint32_t q = threadIdx.x; q < tn; q += blockDim.x) {
+      KT kk = skey[q];
+      unsigned d = (unsigned)((uint64_t)kk >> shift) & 0xffu;
+      uint32_t g = run_off[d] + (q - tstart[d]);
+      kout[g] = kk;
+      vout[g] = sval[q];
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x) run_off[d] += ttot[d];
+    __syncthreads();
+  }
+}
+
+// ---- K3: run-length heads --------------------------------------------------
+template <typename KT>
+struct HeadGen {
+  const KT* keys;
+  __device__ uint32_t operator()(uint64_t i) const {
+    return (i == 0 || keys[i] != keys[i - 1]) ? 1u : 0u;
+  }
+};
+
+struct HeadOut {
+  uint32_t* starts;
+  __device__ void operator()(uint64_t i, uint32_t ex, uint32_t v) const {
+    if (v) starts[ex] = (uint32_t)i;
+  }
+};
+
+// ---- K4: segment reduce (one owner per output term) -------------------------
+template <typename KT, int NL, int CK>
+__global__ void __launch_bounds__(256)
+k_seg_reduce_int(const KT* __restrict__ keys, const uint64_t* __restrict__ vals,
+                 const uint32_t* __restrict__ starts, uint32_t nseg, const void* __restrict__ ac,
+                 const void* __restrict__ bc, uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp,
+                 uint64_t* __restrict__ ocoef, uint32_t* __restrict__ onz) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  uint32_t p0 = starts[s], p1 = starts[s + 1];
+  Limbs<NL> acc;
+  limbs_zero(acc);
+  for (uint32_t p = p0; p < p1; ++p) {
+    uint64_t v = vals[p];
+    ICoef a = load_icoef<CK>(ac, (int64_t)(v >> 32));
+    ICoef b = load_icoef<CK>(bc, (int64_t)(v & 0xffffffffu));
+    limbs_add(acc, imul<NL, CK>(a, b));
+  }
+  oexp[s] = expand_key((uint64_t)keys[p0] + KL, P);
+#pragma unroll
+  for (int k = 0; k < NL; ++k) ocoef[(uint64_t)s * NL + k] = acc.w[k];
+  onz[s] = limbs_nonzero(acc) ? 1u : 0u;
+}
+
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_seg_reduce_f64(const KT* __restrict__ keys, const uint64_t* __restrict__ vals,
+                 const uint32_t* __restrict__ starts, uint32_t nseg, const double* __restrict__ ac,
+                 const double* __restrict__ bc, uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp,
+                 double* __restrict__ ocoef, uint32_t* __restrict__ onz) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  uint32_t p0 = starts[s], p1 = starts[s + 1];
+  uint64_t v = vals[p0];
+  // reference order: acc = a_i*b_j, then acc += a_i'*b_j' for increasing i'
+  double acc = __dmul_rn(__ldg(ac + (v >> 32)), __ldg(bc + (v & 0xffffffffu)));
+  for (uint32_t p = p0 + 1; p < p1; ++p) {
+    v = vals[p];
+    acc = __dadd_rn(acc, __dmul_rn(__ldg(ac + (v >> 32)), __ldg(bc + (v & 0xffffffffu))));
+  }
+  oexp[s] = expand_key((uint64_t)keys[p0] + KL, P);
+  ocoef[s] = acc;
+  onz[s] = (acc != 0.0) ? 1u : 0u;  // NaN != 0 -> kept, +-0 dropped (merge.py:63)
+}
+
+// ---- K5: zero-coefficient compaction ---------------------------------------
+struct FlagGen {
+  const uint32_t* f;
+  __device__ uint32_t operator()(uint64_t i) const { return f[i]; }
+};
+
+struct CompactOut {
+  const uint64_t* iexp;
+  const uint64_t* icoef;   // limbs (f64 viewed as one u64 limb)
+  int nl;
+  uint64_t* oexp;
+  uint64_t* ocoef;
+  __device__ void operator()(uint64_t i, uint32_t ex, uint32_t v) const {
+    if (!v) return;
+    oexp[ex] = iexp[i];
+    for (int k = 0; k < nl; ++k) ocoef[(uint64_t)ex * nl + k] = icoef[i * nl + k];
+  }
+};
+
+}  // namespace pgpu

@@ -1,0 +1,155 @@
+"""Parity of the CUDA library with the reference (through the C ABI).
+
+Integers: bit-exact (exponents, order, coefficients).  Floats: bit-exact in
+float_ordered mode (the reference's summation order); otherwise within the
+rigorous reordering bound |c_gpu - c_ref| <= 2*k*2^-53*sum_j |a_i b_j| with k
+the number of products of the term.
+"""
+
+from __future__ import annotations
+
+import math
+
+import numpy as np
+import pytest
+
+from conftest import digests, golden_cases, product_digest
+from paper_1303_7425_b200 import (CoefficientOverflowError, ExponentOverflowError, MulConfig,
+                                  Polynomial, benchpolys, default_layout, io, mul)
+from paper_1303_7425_b200.parmul import Operand, native_mul
+from paper_1303_7425_b200.split import GridParams, SplitSet, select_grid
+
+pytestmark = pytest.mark.gpu
+CASES = golden_cases()
+
+
+def _check(got, want, ordered_float=True, a=None, b=None):
+    assert got.n == want["n"], f"{got.n} terms vs {want['n']}"
+    if got.ctype is int or ordered_float:
+        assert product_digest(got.exps, got.coeffs) == want["sha256"]
+    elif "exps" in want:
+        assert got.exps == [int(e) for e in want["exps"]]
+
+
+@pytest.mark.parametrize("path", ["auto", "sort"])
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_golden_cases(case, path):
+    name, a, b, split, want = case
+    cfg = MulConfig(path=path, float_ordered=True)
+    got = mul(a, b, cfg, split=None if split is None else SplitSet(split))
+    _check(got, want)
+
+
+@pytest.mark.parametrize("case", [c for c in CASES if c[1].ctype is int], ids=lambda c: c[0])
+def test_golden_cases_dense_when_applicable(case):
+    name, a, b, split, want = case
+    try:
+        got = mul(a, b, MulConfig(path="dense"), split=None if split is None else SplitSet(split))
+    except Exception as exc:  # key span too wide for a bytemap: the dense path refuses loudly
+        assert "dense path" in str(exc)
+        return
+    _check(got, want)
+
+
+@pytest.mark.parametrize("cfg", ["fateman10/int", "fateman20/int", "fateman30/int", "mp12/int",
+                                 "fateman10/float"])
+@pytest.mark.parametrize("path", ["auto", "sort"])
+def test_benchmark_digests(cfg, path):
+    name, kind = cfg.split("/")
+    f, g = benchpolys.CONFIGS[name](float if kind == "float" else int)
+    p = mul(f, g, MulConfig(path=path))
+    want = digests()["products"][cfg]
+    assert p.n == want["n"]
+    assert io.poly_digest(p) == want["sha256"]
+
+
+@pytest.mark.parametrize("cfg", ["fateman20/float", "mp12/float"])
+def test_float_ordered_mode_is_bit_exact(cfg):
+    name, _ = cfg.split("/")
+    f, g = benchpolys.CONFIGS[name](float)
+    p = mul(f, g, MulConfig(float_ordered=True))
+    want = digests()["products"][cfg]
+    assert p.n == want["n"] and io.poly_digest(p) == want["sha256"]
+
+
+@pytest.mark.parametrize("name", ["fateman20", "fateman30", "mp12"])
+def test_float_fast_mode_within_bound(name):
+    f, g = benchpolys.CONFIGS[name](float)
+    fast = mul(f, g, MulConfig(path="auto"))
+    exact = mul(f, g, MulConfig(float_ordered=True))
+    assert fast.exps == exact.exps
+    # all-positive operands: sum|a_i b_j| == the coefficient itself; k <= min(na, nb)
+    k = min(f.n, g.n)
+    x = np.asarray(fast.coeffs)
+    y = np.asarray(exact.coeffs)
+    bound = 2 * k * 2.0 ** -53 * np.abs(y)
+    assert np.all(np.abs(x - y) <= bound)
+
+
+def test_mp25_sampled_intervals_match_reference():
+    """MP n=25 against the reference's digests of sampled intervals
+    (SURVEY.md Appendix A), each interval computed as its own GPU range."""
+    import hashlib
+    d = digests()["mp25_intervals"]
+    f, g = benchpolys.monagan_pearce(25)
+    bounds = select_grid(f, g, GridParams(d["grid_l"])).bounds
+    assert len(bounds) == d["n_s"]
+    A, B = Operand.from_poly(f), Operand.from_poly(g)
+    rows = {r["k"]: r for r in d["rows"]}
+    ks = list(range(0, 4289, 64)) + [4322]
+    combined = hashlib.sha256()
+    for k in ks:
+        raw = native_mul(A, B, f.layout, lo=bounds[k], hi=bounds[k + 1])
+        from paper_1303_7425_b200.parmul import limbs_to_ints
+        co = limbs_to_ints(raw.coef, raw.nl)
+        h = product_digest(raw.exps.tolist(), co)
+        combined.update(h.encode())
+        if k in rows:
+            assert str(bounds[k]) == rows[k]["lo"] or k == 0
+            assert raw.pairs == rows[k]["ops"]
+            assert raw.exps.size == rows[k]["terms"]
+            assert h == rows[k]["sha256"], f"interval {k}"
+    assert combined.hexdigest() == d["combined_sha256"]
+
+
+def test_errors_and_edge_cases():
+    lay = default_layout(("x",))
+    x = Polynomial.variable(lay, "x")
+    with pytest.raises(ValueError):
+        mul(x, Polynomial.variable(default_layout(("y",)), "y"))
+    with pytest.raises(ValueError):
+        mul(x, Polynomial.variable(lay, "x", float))
+    assert mul(x, Polynomial.zero(lay)).is_zero
+    assert mul(Polynomial.zero(lay), Polynomial.zero(lay)).is_zero
+    top = Polynomial(lay, [(1, (lay.max_vector()[0],))])
+    with pytest.raises(ExponentOverflowError):
+        mul(top, x)
+    # (1+x)^2 with a split starting at x: the constant term is not formed
+    one_x = Polynomial.constant(lay, 1) + x
+    p = mul(one_x, one_x, split=SplitSet([lay.pack((1,)), (1 << 64) - 1]))
+    assert p.coeffs == [2, 1] and p.exps == [lay.pack((1,)), lay.pack((2,))]
+
+
+def test_coefficient_width_selection_and_overflow_guard():
+    lay = default_layout(("x", "y"))
+    a = Polynomial(lay, [((1 << 126) - 1, (1, 0)), (-(1 << 126), (0, 1))])
+    # the bound needs 126+126+2 bits > 192 -> refused before launch, never wrapped
+    with pytest.raises(CoefficientOverflowError):
+        mul(a, a)
+    b = Polynomial(lay, [((1 << 80) + 1, (1, 0)), (-(1 << 70), (0, 1))])
+    c = Polynomial(lay, [(3, (1, 1)), (-7, (2, 0))])
+    want = {}
+    for ea, ca in zip(b.exps, b.coeffs):
+        for ec, cc in zip(c.exps, c.coeffs):
+            want[ea + ec] = want.get(ea + ec, 0) + ca * cc
+    got = mul(b, c)
+    assert got.exps == sorted(k for k, v in want.items() if v)
+    assert got.coeffs == [want[e] for e in got.exps]
+
+
+def test_result_class_follows_operand_class():
+    lay = default_layout(("x", "y"))
+    a = Polynomial(lay, [(3, (1, 0)), (5, (0, 1))])
+    p = mul(a, a)
+    assert type(p) is Polynomial
+    p.validate()
