@@ -11,22 +11,25 @@
 //                             set is exactly the marked keys, ascending.
 //             D2 k_words      bytemap -> bit words + exclusive rank prefix
 //                             (device scan) + the ascending output key list.
-//   numeric   D3 k_edges_multi  per interval bound, each row's column bound
-//                             (find_edge, split.py:131-166) by two-pointer walks.
-//             D4 k_numeric    one CTA per (interval, row block).  Interval =
-//                             D consecutive output terms.  Each warp owns a
-//                             private accumulator copy in shared memory and
-//                             walks one row at a time with lanes on consecutive
-//                             columns: keys of one row are distinct, so no two
-//                             lanes touch the same slot -- no atomics, no locks
-//                             (the paper's independent-term property).  The
-//                             slot of a pair is its output rank (bit words +
-//                             prefix).  Warps' copies are folded by one owner
-//                             thread per output term.
-//             D5 k_fold       (row-blocked intervals) one owner per output
-//                             term sums the row blocks' partials, tests zero
-//                             (merge.py:63) and writes the exponent.
+//   numeric   D4 k_numeric    one CTA per (row block, segment of consecutive
+//                             intervals).  Interval = D consecutive output
+//                             terms.  Each row keeps a cursor, so its run in
+//                             the next interval is found by walking forward
+//                             (find_edge, split.py:131-166, amortised to one
+//                             comparison per pair).  Each warp owns a private
+//                             accumulator copy in shared memory and walks one
+//                             row at a time with lanes on consecutive columns:
+//                             keys of one row are distinct, so no two lanes
+//                             touch the same slot -- no atomics, no locks (the
+//                             paper's independent-term property).  A pair's
+//                             slot is its output rank (bit words + prefix, or a
+//                             per-interval shared-memory table).  One owner
+//                             thread per output term folds the warps' copies.
+//             D5 k_fold       one owner per output term sums the row blocks'
+//                             partials, tests zero (merge.py:63) and writes the
+//                             exponent.
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -108,63 +111,122 @@ struct WordOut {
   }
 };
 
-// ---- D3 ---------------------------------------------------------------------
-// E[t*na + i] = #{j : ak[i] + bk[j] < bound_t}, bound_t = okey[t*D] (t < T),
-// bound_T = R1.  One thread walks kEdgeRun consecutive rows: a binary search
-// for the first row, then the column pointer only moves left.
-constexpr int kEdgeRun = 16;
-
+// ---- D3/D4 -------------------------------------------------------------------
+// Interval t = output ranks [t*D, (t+1)*D); bound_t = okey[t*D], bound_T = R1.
 template <typename KT>
 __device__ __forceinline__ uint64_t interval_bound(const KT* okey, uint32_t t, uint32_t T, uint32_t D,
                                                    uint64_t R1) {
   return t < T ? (uint64_t)okey[(uint64_t)t * D] : R1;
 }
 
-template <typename KT>
-__global__ void __launch_bounds__(256)
-k_edges_multi(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk, uint32_t nb,
-              const KT* __restrict__ okey, uint32_t T, uint32_t D, uint64_t R1,
-              uint32_t* __restrict__ E, uint32_t t_off) {
-  const uint32_t t = blockIdx.y + t_off;
-  const uint64_t K = interval_bound(okey, t, T, D, R1);
-  const uint32_t nchunks = (na + kEdgeRun - 1) / kEdgeRun;
-  for (uint32_t ch = blockIdx.x * blockDim.x + threadIdx.x; ch < nchunks;
-       ch += gridDim.x * blockDim.x) {
-    uint32_t i0 = ch * kEdgeRun, i1 = min(i0 + kEdgeRun, na);
-    uint32_t c = count_below(bk, nb, (uint64_t)ak[i0], K);
-    uint32_t* e = E + (uint64_t)t * na;
-    e[i0] = c;
-    for (uint32_t i = i0 + 1; i < i1; ++i) {
-      uint64_t ai = ak[i];
-      while (c > 0 && ai + (uint64_t)bk[c - 1] >= K) --c;
-      e[i] = c;
+constexpr int kNumWarps = 8;
+constexpr int kNumThreads = kNumWarps * 32;
+constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot table
+constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
+constexpr size_t kAccBytes = 80 * 1024;
+constexpr int kUnroll = 2;           // independent columns per lane per step
+
+// Accumulator geometry.  NW = words of a finished term.  CB = 1: the term is
+// held as 4 word planes plus a one-byte carry counter (nonnegative products
+// below 2^128 and a proven bound <= 136 bits: at most 255 carries per copy),
+// else as NW word planes.  D = terms per interval.
+template <int NW, int CB>
+struct Geo {
+  static constexpr int NP = CB ? 4 : NW;                 // u32 planes
+  static constexpr uint32_t D =
+      (uint32_t)(kAccBytes / (kNumWarps * (NP * 4 + CB))) / 32 * 32 - 32;
+  static constexpr uint32_t DP = D + 32;                 // + one pad slot per lane
+  static constexpr uint32_t stride = kNumWarps * DP;     // words between planes
+  static constexpr size_t tbl_off = (size_t)NP * stride * 4 + (CB ? (stride + 15) / 16 * 16 : 0);
+  static constexpr size_t smem = tbl_off + kTbl * 2;
+};
+
+// MODE: 0 f64 (NW = 2: one double), 1 int64 with all coefficients >= 0
+//       (unsigned products, carry into words >= 4 only when it happens),
+//       2 int64 signed, 3 int128 signed.
+struct NumArgs {
+  const void* ak;
+  const void* bk;    // padded with kUnroll*32 entries past nb
+  const void* ac;
+  const void* bc;
+  uint32_t na, nb;
+  const uint32_t* bits;
+  const uint32_t* prefix;
+  uint64_t R0, R1;
+  const void* okey;
+  uint32_t nout, D, T, R, S;
+  uint32_t* cursor;  // [S][na]: next column of each row for this interval segment
+  void* nextkey;     // [S][na]: key at that column (KT; all-ones when exhausted)
+  void* partial;     // [T][R][D][NW] words (R > 1)
+  int nl;
+  uint64_t* oexp;
+  uint64_t* ocoef;
+  uint32_t* onz;
+};
+
+// Finished term: NW words -> nl sign-extended u64 limbs + nonzero flag.
+template <int NW, int MODE>
+__device__ __forceinline__ void write_term(const NumArgs& A, uint32_t o, const uint32_t (&v)[NW]) {
+  const uint32_t ext = MODE == 1 ? 0u : (uint32_t)((int32_t)v[NW - 1] >> 31);
+  uint32_t nzv = 0;
+#pragma unroll
+  for (int k = 0; k < NW; ++k) nzv |= v[k];
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    if (k < A.nl) {
+      const uint32_t lo = 2 * k < NW ? v[2 * k < NW ? 2 * k : 0] : ext;
+      const uint32_t hi = 2 * k + 1 < NW ? v[2 * k + 1 < NW ? 2 * k + 1 : 0] : ext;
+      A.ocoef[(uint64_t)o * A.nl + k] = (uint64_t)lo | ((uint64_t)hi << 32);
     }
   }
+  A.onz[o] = nzv ? 1u : 0u;
 }
 
-// ---- D4 ---------------------------------------------------------------------
-constexpr int kNumThreads = 256;
-constexpr int kNumWarps = kNumThreads / 32;
-
-// Shared-memory accumulator words: acc[word][warp][slot] (u32), NW words per
-// term (int), or a double per (warp, slot) for f64.
-template <int NW, int CK>
-__device__ __forceinline__ void words_of_product(const ICoef& a, const ICoef& b, uint32_t (&p)[NW]) {
-  constexpr int NL = (NW + 1) / 2;
-  Limbs<NL> r = imul<NL, CK>(a, b);
+// acc[k*stride] += p (little-endian words, modulo 2^(32 NW))
+template <int NW, uint32_t STRIDE>
+__device__ __forceinline__ void add_words(uint32_t* a, const uint32_t (&p)[NW]) {
+  uint32_t v[NW];
 #pragma unroll
-  for (int k = 0; k < NW; ++k) p[k] = (uint32_t)(r.w[k >> 1] >> (32 * (k & 1)));
-}
-
-template <int NW>
-__device__ __forceinline__ void smem_add_words(uint32_t* acc, uint32_t stride, const uint32_t (&p)[NW]) {
-  uint64_t c = 0;
-#pragma unroll
-  for (int k = 0; k < NW; ++k) {
-    uint64_t s = (uint64_t)acc[k * stride] + p[k] + c;
-    acc[k * stride] = (uint32_t)s;
-    c = s >> 32;
+  for (int k = 0; k < NW; ++k) v[k] = a[k * STRIDE];
+  if constexpr (NW == 2) {
+    asm("add.cc.u32 %0, %0, %2;\n\taddc.u32 %1, %1, %3;" : "+r"(v[0]), "+r"(v[1]) : "r"(p[0]), "r"(p[1]));
+  } else if constexpr (NW == 3) {
+    asm("add.cc.u32 %0, %0, %3;\n\taddc.cc.u32 %1, %1, %4;\n\taddc.u32 %2, %2, %5;"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]) : "r"(p[0]), "r"(p[1]), "r"(p[2]));
+  } else if constexpr (NW == 4) {
+    asm("add.cc.u32 %0, %0, %4;\n\taddc.cc.u32 %1, %1, %5;\n\taddc.cc.u32 %2, %2, %6;\n\t"
+        "addc.u32 %3, %3, %7;"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3])
+        : "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]));
+  } else if constexpr (NW == 5) {
+    asm("add.cc.u32 %0, %0, %5;\n\taddc.cc.u32 %1, %1, %6;\n\taddc.cc.u32 %2, %2, %7;\n\t"
+        "addc.cc.u32 %3, %3, %8;\n\taddc.u32 %4, %4, %9;"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4])
+        : "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]));
+  } else {
+    asm("add.cc.u32 %0, %0, %6;\n\taddc.cc.u32 %1, %1, %7;\n\taddc.cc.u32 %2, %2, %8;\n\t"
+        "addc.cc.u32 %3, %3, %9;\n\taddc.cc.u32 %4, %4, %10;\n\taddc.u32 %5, %5, %11;"
+        : "+r"(v[0]), "+r"(v[1]), "+r"(v[2]), "+r"(v[3]), "+r"(v[4]), "+r"(v[5])
+        : "r"(p[0]), "r"(p[1]), "r"(p[2]), "r"(p[3]), "r"(p[4]), "r"(p[5]));
   }
+#pragma unroll
+  for (int k = 0; k < NW; ++k) a[k * STRIDE] = v[k];
+}
+
+// Unsigned 128-bit product into 4 word planes; the carry out of bit 128 bumps
+// the slot's byte counter (rare: only when the copy crosses a 2^128 multiple).
+template <uint32_t STRIDE>
+__device__ __forceinline__ void add_unsigned128(uint32_t* a, uint8_t* carry, uint64_t lo, uint64_t hi) {
+  uint32_t v0 = a[0], v1 = a[STRIDE], v2 = a[2 * STRIDE], v3 = a[3 * STRIDE], cy;
+  asm("add.cc.u32 %0, %0, %5;\n\taddc.cc.u32 %1, %1, %6;\n\taddc.cc.u32 %2, %2, %7;\n\t"
+      "addc.cc.u32 %3, %3, %8;\n\taddc.u32 %4, 0, 0;"
+      : "+r"(v0), "+r"(v1), "+r"(v2), "+r"(v3), "=r"(cy)
+      : "r"((uint32_t)lo), "r"((uint32_t)(lo >> 32)), "r"((uint32_t)hi), "r"((uint32_t)(hi >> 32)));
+  a[0] = v0;
+  a[STRIDE] = v1;
+  a[2 * STRIDE] = v2;
+  a[3 * STRIDE] = v3;
+  if (cy) *carry += 1;
 }
 
 template <typename KT>
@@ -175,202 +237,266 @@ __device__ __forceinline__ uint32_t rank_of(uint64_t klocal, const uint32_t* __r
   return __ldg(prefix + w) + __popc(m);
 }
 
-// Accumulate one (interval, row block) unit.  Output: if `final_out`, the
-// owner thread writes the finished term; else the unit's partial words.
-template <typename KT, int NW, int CK>
+// One CTA = (row block r, interval segment s).  Intervals of the segment are
+// processed in ascending order; each row keeps a cursor (first column whose key
+// is >= the current interval's lower bound), so a row's run in interval t is
+// found by walking forward from its cursor -- no per-interval edge search.
+template <typename KT, int NW, int MODE, int CB>
 __global__ void __launch_bounds__(kNumThreads)
-k_numeric_int(const KT* __restrict__ ak, const KT* __restrict__ bk, const void* __restrict__ ac,
-              const void* __restrict__ bc, uint32_t na, const uint32_t* __restrict__ E,
-              const uint32_t* __restrict__ bits, const uint32_t* __restrict__ prefix, uint64_t R0,
-              uint32_t nout, uint32_t D, uint32_t R, uint32_t* __restrict__ partial,
-              const KT* __restrict__ okey, KeyPlan P, int nl, uint64_t* __restrict__ oexp,
-              uint64_t* __restrict__ ocoef, uint32_t* __restrict__ onz) {
-  extern __shared__ uint32_t sacc[];  // [NW][kNumWarps][D]
-  const uint32_t t = blockIdx.x / R, r = blockIdx.x % R;
-  const uint32_t base = t * D;
-  const uint32_t dcount = min(D, nout - base);
-  const uint32_t stride = kNumWarps * D;
-  for (uint32_t k = threadIdx.x; k < NW * stride; k += blockDim.x) sacc[k] = 0;
-  __syncthreads();
+k_numeric(NumArgs A) {
+  using G = Geo<NW, CB>;
+  constexpr uint32_t D = G::D;
+  constexpr uint32_t DP = G::DP;
+  constexpr uint32_t STRIDE = G::stride;
+  constexpr int NP = G::NP;
+  extern __shared__ __align__(16) uint32_t smem_u32[];
+  uint32_t* acc = smem_u32;                                        // [NP][W][D]
+  uint8_t* cbyte = reinterpret_cast<uint8_t*>(acc + NP * STRIDE);  // [W][D] (CB)
+  uint16_t* tbl = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(smem_u32) + G::tbl_off);
+  const KT* __restrict__ ak = (const KT*)A.ak;
+  const KT* __restrict__ bk = (const KT*)A.bk;
+  const KT* __restrict__ okey = (const KT*)A.okey;
+  const uint32_t r = blockIdx.x % A.R, s = blockIdx.x / A.R;
+  const uint32_t t_begin = (uint32_t)((uint64_t)A.T * s / A.S);
+  const uint32_t t_end = (uint32_t)((uint64_t)A.T * (s + 1) / A.S);
+  const uint32_t rb0 = (uint32_t)((uint64_t)A.na * r / A.R);
+  const uint32_t rb1 = (uint32_t)((uint64_t)A.na * (r + 1) / A.R);
+  uint32_t* cur = A.cursor + (uint64_t)s * A.na;
+  KT* nk = (KT*)A.nextkey + (uint64_t)s * A.na;
+  const KT kInf = (KT)~(KT)0;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t rb0 = (uint32_t)((uint64_t)na * r / R), rb1 = (uint32_t)((uint64_t)na * (r + 1) / R);
-  const uint32_t* e0 = E + (uint64_t)t * na;
-  const uint32_t* e1 = e0 + na;
-  uint32_t* my = sacc + w * D;
-  // warps take 32-row groups round robin; inside a group, one row at a time
-  for (uint32_t g = rb0 + w * 32; g < rb1; g += kNumWarps * 32) {
-    uint32_t i = g + lane;
-    uint32_t lo = 0, hi = 0;
-    if (i < rb1) {
-      lo = e0[i];
-      hi = e1[i];
-    }
-    unsigned todo = __ballot_sync(0xffffffffu, hi > lo);
-    while (todo) {
-      int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      uint32_t ri = g + src;
-      uint32_t jlo = __shfl_sync(0xffffffffu, lo, src);
-      uint32_t jhi = __shfl_sync(0xffffffffu, hi, src);
-      uint64_t a = (uint64_t)ak[ri] - R0;
-      ICoef ca = load_icoef<CK>(ac, ri);
-      for (uint32_t j = jlo + lane; j < jhi; j += 32) {
-        uint64_t kl = a + (uint64_t)bk[j];
-        uint32_t slot = rank_of<KT>(kl, bits, prefix) - base;
-        ICoef cb = load_icoef<CK>(bc, j);
-        uint32_t p[NW];
-        words_of_product<NW, CK>(ca, cb, p);
-        smem_add_words<NW>(my + slot, stride, p);
+  const uint32_t nb = A.nb;
+  if (t_begin >= t_end) return;
+  {  // cursors at the segment's first bound: binary search, then walk left
+    const uint64_t K0 = interval_bound(okey, t_begin, A.T, D, A.R1);
+    const uint32_t nrow = rb1 - rb0;
+    for (uint32_t ch = threadIdx.x; ch * kCursorRun < nrow; ch += blockDim.x) {
+      uint32_t i0 = rb0 + ch * kCursorRun, i1 = min(i0 + kCursorRun, rb1);
+      uint32_t c = count_below(bk, nb, (uint64_t)ak[i0], K0);
+      for (uint32_t i = i0; i < i1; ++i) {
+        uint64_t ai = ak[i];
+        if (i > i0)
+          while (c > 0 && ai + (uint64_t)bk[c - 1] >= K0) --c;
+        cur[i] = c;
+        nk[i] = c < nb ? (KT)(ai + (uint64_t)bk[c]) : kInf;
       }
-      __syncwarp();
     }
   }
   __syncthreads();
-  // one owner thread per output slot folds the warps' copies
-  for (uint32_t s = threadIdx.x; s < dcount; s += blockDim.x) {
-    uint32_t v[NW];
-#pragma unroll
-    for (int k = 0; k < NW; ++k) v[k] = 0;
-#pragma unroll 1
-    for (int q = 0; q < kNumWarps; ++q) {
-      uint32_t p[NW];
-#pragma unroll
-      for (int k = 0; k < NW; ++k) p[k] = sacc[k * stride + q * D + s];
-      uint64_t c = 0;
-#pragma unroll
-      for (int k = 0; k < NW; ++k) {
-        uint64_t x = (uint64_t)v[k] + p[k] + c;
-        v[k] = (uint32_t)x;
-        c = x >> 32;
+  for (uint32_t t = t_begin; t < t_end; ++t) {
+    const uint64_t Klo = interval_bound(okey, t, A.T, D, A.R1);
+    const uint64_t Khi = interval_bound(okey, t + 1, A.T, D, A.R1);
+    const KT kmax = (KT)(Khi - 1);  // keys of the interval: [Klo, kmax]
+    const uint32_t base = t * D;
+    const uint32_t dcount = min(D, A.nout - base);
+    const bool use_tbl = (Khi - Klo) <= kTbl;
+    for (uint32_t k = threadIdx.x; k < G::tbl_off / 4; k += blockDim.x) acc[k] = 0;
+    if (use_tbl) {
+      const uint64_t w0 = (Klo - A.R0) >> 5, w1 = (Khi - 1 - A.R0) >> 5;
+      for (uint64_t wd = w0 + threadIdx.x; wd <= w1; wd += blockDim.x) {
+        uint32_t m = __ldg(A.bits + wd);
+        uint32_t rk = __ldg(A.prefix + wd) - base;
+        while (m) {
+          int b = __ffs(m) - 1;
+          m &= m - 1;
+          uint64_t k = A.R0 + wd * 32 + b;
+          if (k >= Klo && k < Khi) tbl[k - Klo] = (uint16_t)rk;
+          ++rk;
+        }
       }
     }
-    if (R == 1) {
-      uint32_t o = base + s;
-      uint64_t nzv = 0;
-      for (int k = 0; k < nl; ++k) {
-        uint32_t lo = 2 * k < NW ? v[2 * k] : (uint32_t)((int32_t)v[NW - 1] >> 31);
-        uint32_t hi = 2 * k + 1 < NW ? v[2 * k + 1] : (uint32_t)((int32_t)v[NW - 1] >> 31);
-        uint64_t limb = (uint64_t)lo | ((uint64_t)hi << 32);
-        ocoef[(uint64_t)o * nl + k] = limb;
+    __syncthreads();
+    uint32_t* my = acc + w * DP;
+    uint8_t* myc = cbyte + w * DP;
+    // one step: kUnroll columns per lane of row (akr, a0/ad) from cursor c; invalid
+    // lanes add into their private pad slot so the step has no divergent branch
+    auto step = [&](const KT akr, const uint64_t a0, const double ad, const uint32_t ri,
+                    const uint32_t c, auto tbl_mode) -> uint32_t {
+      constexpr bool TBL = decltype(tbl_mode)::value;
+      uint32_t nv = 0;
+      uint32_t slot[kUnroll];
+      uint32_t jj[kUnroll];
+      bool okk[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t j = c + lane + 32 * u;
+        const KT key = (KT)(akr + bk[j]);  // bk is padded: the load is in bounds
+        const bool ok = j < nb && key <= kmax;
+        nv += __popc(__ballot_sync(0xffffffffu, ok));
+        uint32_t sl;
+        if constexpr (TBL) {
+          sl = tbl[ok ? (uint32_t)(key - (KT)Klo) : 0u];
+        } else {
+          sl = ok ? rank_of<KT>((uint64_t)key - A.R0, A.bits, A.prefix) - base : 0u;
+        }
+        slot[u] = ok ? sl : D + lane;
+        jj[u] = ok ? j : 0u;
+        okk[u] = ok;
       }
 #pragma unroll
-      for (int k = 0; k < NW; ++k) nzv |= v[k];
-      onz[o] = nzv ? 1u : 0u;
-      oexp[o] = expand_key((uint64_t)okey[o], P);
-    } else {
-      uint32_t* dst = partial + ((uint64_t)blockIdx.x * D + s) * NW;
+      for (int u = 0; u < kUnroll; ++u) {
+        const uint32_t j = jj[u];
+        if constexpr (MODE == 0) {
+          double* d = reinterpret_cast<double*>(acc) + w * DP + slot[u];
+          const double bv = okk[u] ? __ldg(reinterpret_cast<const double*>(A.bc) + j) : 0.0;
+          *d = __dadd_rn(*d, __dmul_rn(ad, bv));
+        } else if constexpr (MODE == 1) {
+          const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
+          const uint64_t lo = a0 * b0;
+          if constexpr (CB) {
+            add_unsigned128<STRIDE>(my + slot[u], myc + slot[u], lo, __umul64hi(a0, b0));
+          } else {
+            uint32_t p[NW];
+            const uint64_t hi = __umul64hi(a0, b0);
+            const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
 #pragma unroll
-      for (int k = 0; k < NW; ++k) dst[k] = v[k];
-    }
-  }
-}
-
-template <typename KT>
-__global__ void __launch_bounds__(kNumThreads)
-k_numeric_f64(const KT* __restrict__ ak, const KT* __restrict__ bk, const double* __restrict__ ac,
-              const double* __restrict__ bc, uint32_t na, const uint32_t* __restrict__ E,
-              const uint32_t* __restrict__ bits, const uint32_t* __restrict__ prefix, uint64_t R0,
-              uint32_t nout, uint32_t D, uint32_t R, double* __restrict__ partial,
-              const KT* __restrict__ okey, KeyPlan P, uint64_t* __restrict__ oexp,
-              double* __restrict__ ocoef, uint32_t* __restrict__ onz) {
-  extern __shared__ double sdacc[];  // [kNumWarps][D]
-  const uint32_t t = blockIdx.x / R, r = blockIdx.x % R;
-  const uint32_t base = t * D;
-  const uint32_t dcount = min(D, nout - base);
-  for (uint32_t k = threadIdx.x; k < kNumWarps * D; k += blockDim.x) sdacc[k] = 0.0;
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  const uint32_t rb0 = (uint32_t)((uint64_t)na * r / R), rb1 = (uint32_t)((uint64_t)na * (r + 1) / R);
-  const uint32_t* e0 = E + (uint64_t)t * na;
-  const uint32_t* e1 = e0 + na;
-  double* my = sdacc + w * D;
-  for (uint32_t g = rb0 + w * 32; g < rb1; g += kNumWarps * 32) {
-    uint32_t i = g + lane;
-    uint32_t lo = 0, hi = 0;
-    if (i < rb1) {
-      lo = e0[i];
-      hi = e1[i];
-    }
-    unsigned todo = __ballot_sync(0xffffffffu, hi > lo);
-    while (todo) {
-      int src = __ffs(todo) - 1;
-      todo &= todo - 1;
-      uint32_t ri = g + src;
-      uint32_t jlo = __shfl_sync(0xffffffffu, lo, src);
-      uint32_t jhi = __shfl_sync(0xffffffffu, hi, src);
-      uint64_t a = (uint64_t)ak[ri] - R0;
-      double ca = __ldg(ac + ri);
-      for (uint32_t j = jlo + lane; j < jhi; j += 32) {
-        uint64_t kl = a + (uint64_t)bk[j];
-        uint32_t slot = rank_of<KT>(kl, bits, prefix) - base;
-        my[slot] = __dadd_rn(my[slot], __dmul_rn(ca, __ldg(bc + j)));
+            for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : 0u;
+            add_words<NW, STRIDE>(my + slot[u], p);
+          }
+        } else if constexpr (MODE == 2) {
+          const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
+          const uint64_t lo = a0 * b0;
+          const uint64_t hi = (uint64_t)__mul64hi((long long)a0, (long long)b0);
+          const uint32_t ext = (uint32_t)((int64_t)hi >> 63);
+          const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
+          uint32_t p[NW];
+#pragma unroll
+          for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : ext;
+          add_words<NW, STRIDE>(my + slot[u], p);
+        } else {
+          ICoef ca = load_icoef<2>(A.ac, ri);
+          ICoef cb = load_icoef<2>(A.bc, j);
+          if (!okk[u]) cb.x0 = cb.x1 = cb.x2 = 0;
+          Limbs<3> pr = imul<3, 2>(ca, cb);
+          uint32_t p[NW];
+#pragma unroll
+          for (int k = 0; k < NW; ++k) p[k] = (uint32_t)(pr.w[k >> 1] >> (32 * (k & 1)));
+          add_words<NW, STRIDE>(my + slot[u], p);
+        }
       }
-      __syncwarp();
+      return nv;
+    };
+    auto rows = [&](auto tbl_mode) {
+      for (uint32_t g = rb0 + w * 32; g < rb1; g += kNumWarps * 32) {
+        const uint32_t i = g + lane;
+        const bool rowok = i < rb1;
+        uint32_t ci = rowok ? cur[i] : 0u;
+        KT nki = rowok ? nk[i] : kInf;
+        unsigned todo = __ballot_sync(0xffffffffu, (uint64_t)nki < Khi);
+        if (!todo) continue;
+        const KT akl = rowok ? ak[i] : (KT)0;
+        uint64_t a0l = 0;
+        double adl = 0.0;
+        if constexpr (MODE == 0) adl = rowok ? __ldg(reinterpret_cast<const double*>(A.ac) + i) : 0.0;
+        else if constexpr (MODE != 3) a0l = rowok ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.ac) + i) : 0ull;
+        while (todo) {
+          const int src = __ffs(todo) - 1;
+          todo &= todo - 1;
+          uint32_t c = __shfl_sync(0xffffffffu, ci, src);
+          const KT akr = __shfl_sync(0xffffffffu, akl, src);
+          const uint64_t a0 = __shfl_sync(0xffffffffu, a0l, src);
+          const double ad = __shfl_sync(0xffffffffu, adl, src);
+          for (;;) {
+            const uint32_t nv = step(akr, a0, ad, g + src, c, tbl_mode);
+            c += nv;
+            if (nv < 32u * kUnroll) break;
+          }
+          if (lane == src) {
+            ci = c;
+            nki = c < nb ? (KT)(akr + bk[c]) : kInf;
+          }
+          __syncwarp();
+        }
+        if (rowok) {
+          cur[i] = ci;
+          nk[i] = nki;
+        }
+      }
+    };
+    if (use_tbl) rows(std::integral_constant<bool, true>{});
+    else rows(std::integral_constant<bool, false>{});
+    __syncthreads();
+    // one owner thread per output slot folds the warps' private copies
+    for (uint32_t sl = threadIdx.x; sl < dcount; sl += blockDim.x) {
+      const uint32_t o = base + sl;
+      if constexpr (MODE == 0) {
+        const double* dacc = reinterpret_cast<const double*>(acc);
+        double v = 0.0;
+#pragma unroll
+        for (int q = 0; q < kNumWarps; ++q) v = __dadd_rn(v, dacc[q * DP + sl]);
+        if (A.R == 1) {
+          reinterpret_cast<double*>(A.ocoef)[o] = v;
+          A.onz[o] = v != 0.0 ? 1u : 0u;
+        } else {
+          reinterpret_cast<double*>(A.partial)[((uint64_t)t * A.R + r) * D + sl] = v;
+        }
+      } else {
+        uint32_t v[NW];
+#pragma unroll
+        for (int k = 0; k < NW; ++k)
+          v[k] = k < NP ? acc[k * STRIDE + sl] : (k == 4 && CB ? (uint32_t)cbyte[sl] : 0u);
+#pragma unroll
+        for (int q = 1; q < kNumWarps; ++q) {
+          uint32_t pw[NW];
+#pragma unroll
+          for (int k = 0; k < NW; ++k)
+            pw[k] = k < NP ? acc[k * STRIDE + q * DP + sl] : (k == 4 && CB ? (uint32_t)cbyte[q * DP + sl] : 0u);
+          uint64_t cy = 0;
+#pragma unroll
+          for (int k = 0; k < NW; ++k) {
+            uint64_t x = (uint64_t)v[k] + pw[k] + cy;
+            v[k] = (uint32_t)x;
+            cy = x >> 32;
+          }
+        }
+        if (A.R == 1) {
+          write_term<NW, MODE>(A, o, v);
+        } else {
+          uint32_t* dst = reinterpret_cast<uint32_t*>(A.partial) + (((uint64_t)t * A.R + r) * D + sl) * NW;
+#pragma unroll
+          for (int k = 0; k < NW; ++k) dst[k] = v[k];
+        }
+      }
     }
-  }
-  __syncthreads();
-  for (uint32_t s = threadIdx.x; s < dcount; s += blockDim.x) {
-    double v = 0.0;
-#pragma unroll 1
-    for (int q = 0; q < kNumWarps; ++q) v = __dadd_rn(v, sdacc[q * D + s]);
-    if (R == 1) {
-      uint32_t o = base + s;
-      ocoef[o] = v;
-      onz[o] = v != 0.0 ? 1u : 0u;
-      oexp[o] = expand_key((uint64_t)okey[o], P);
-    } else {
-      partial[(uint64_t)blockIdx.x * D + s] = v;
-    }
+    __syncthreads();
   }
 }
 
 // ---- D5 ---------------------------------------------------------------------
-template <typename KT, int NW>
+// One owner per output term: sums the row blocks' partials, zero test
+// (merge.py:63), output exponent from its key.
+template <typename KT, int NW, int MODE>
 __global__ void __launch_bounds__(256)
-k_fold_int(const uint32_t* __restrict__ partial, uint32_t nout, uint32_t D, uint32_t R,
-           const KT* __restrict__ okey, KeyPlan P, int nl, uint64_t* __restrict__ oexp,
-           uint64_t* __restrict__ ocoef, uint32_t* __restrict__ onz) {
-  uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= nout) return;
-  uint32_t t = o / D, s = o % D;
-  uint32_t v[NW];
+k_fold(NumArgs A, KeyPlan P) {
+  const uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
+  if (o >= A.nout) return;
+  const uint32_t t = o / A.D, sl = o % A.D;
+  if (A.R > 1) {
+    if constexpr (MODE == 0) {
+      double v = 0.0;
+      for (uint32_t r = 0; r < A.R; ++r)
+        v = __dadd_rn(v, reinterpret_cast<const double*>(A.partial)[((uint64_t)t * A.R + r) * A.D + sl]);
+      reinterpret_cast<double*>(A.ocoef)[o] = v;
+      A.onz[o] = v != 0.0 ? 1u : 0u;
+    } else {
+      uint32_t v[NW];
 #pragma unroll
-  for (int k = 0; k < NW; ++k) v[k] = 0;
-  for (uint32_t r = 0; r < R; ++r) {
-    const uint32_t* src = partial + ((uint64_t)(t * R + r) * D + s) * NW;
-    uint64_t c = 0;
+      for (int k = 0; k < NW; ++k) v[k] = 0;
+      for (uint32_t r = 0; r < A.R; ++r) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(A.partial) +
+                              (((uint64_t)t * A.R + r) * A.D + sl) * NW;
+        uint64_t cy = 0;
 #pragma unroll
-    for (int k = 0; k < NW; ++k) {
-      uint64_t x = (uint64_t)v[k] + src[k] + c;
-      v[k] = (uint32_t)x;
-      c = x >> 32;
+        for (int k = 0; k < NW; ++k) {
+          uint64_t x = (uint64_t)v[k] + src[k] + cy;
+          v[k] = (uint32_t)x;
+          cy = x >> 32;
+        }
+      }
+      write_term<NW, MODE>(A, o, v);
     }
   }
-  uint64_t nzv = 0;
-  for (int k = 0; k < nl; ++k) {
-    uint32_t lo = 2 * k < NW ? v[2 * k] : (uint32_t)((int32_t)v[NW - 1] >> 31);
-    uint32_t hi = 2 * k + 1 < NW ? v[2 * k + 1] : (uint32_t)((int32_t)v[NW - 1] >> 31);
-    ocoef[(uint64_t)o * nl + k] = (uint64_t)lo | ((uint64_t)hi << 32);
-  }
-#pragma unroll
-  for (int k = 0; k < NW; ++k) nzv |= v[k];
-  onz[o] = nzv ? 1u : 0u;
-  oexp[o] = expand_key((uint64_t)okey[o], P);
-}
-
-template <typename KT>
-__global__ void __launch_bounds__(256)
-k_fold_f64(const double* __restrict__ partial, uint32_t nout, uint32_t D, uint32_t R,
-           const KT* __restrict__ okey, KeyPlan P, uint64_t* __restrict__ oexp,
-           double* __restrict__ ocoef, uint32_t* __restrict__ onz) {
-  uint32_t o = blockIdx.x * blockDim.x + threadIdx.x;
-  if (o >= nout) return;
-  uint32_t t = o / D, s = o % D;
-  double v = 0.0;
-  for (uint32_t r = 0; r < R; ++r) v = __dadd_rn(v, partial[(uint64_t)(t * R + r) * D + s]);
-  ocoef[o] = v;
-  onz[o] = v != 0.0 ? 1u : 0u;
-  oexp[o] = expand_key((uint64_t)okey[o], P);
+  A.oexp[o] = expand_key((uint64_t)((const KT*)A.okey)[o], P);
 }
 
 }  // namespace pgpu

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
@@ -179,6 +180,7 @@ struct Problem {
   int ck;          // coefficient kind
   int nl;          // integer result limbs (0 for f64)
   int need_bits;   // proven bound on |coefficient| bits + sign
+  bool nonneg;     // no negative operand coefficient (unsigned products)
   KeyPlan P;
   bool k32;        // keys fit 32 bits
   void* ak;        // compact keys (uint32_t* or uint64_t*)
@@ -472,20 +474,32 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   TRY(ctx.ar->alloc(&dst, 1));
   CUDA_TRY(cudaMemsetAsync(dst, 0, sizeof(OperandStats), ctx.st));
   int ga = grid_for(pb.na, 256, ctx.sms * 4), gb = grid_for(pb.nb, 256, ctx.sms * 4);
+  double* dsum;
+  TRY(ctx.ar->alloc(&dsum, ga + gb));
   if (o.coef_kind == PGPU_F64) {
-    k_stats<0><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0);
-    k_stats<0><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1);
+    k_stats<0><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0, dsum);
+    k_stats<0><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1, dsum + ga);
   } else if (o.coef_kind == PGPU_I64) {
-    k_stats<1><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0);
-    k_stats<1><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1);
+    k_stats<1><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0, dsum);
+    k_stats<1><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1, dsum + ga);
   } else {
-    k_stats<2><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0);
-    k_stats<2><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1);
+    k_stats<2><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.acoef, pb.na, P, dst, 0, dsum);
+    k_stats<2><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1, dsum + ga);
   }
   LAUNCHED(2);
   OperandStats hs;
+  std::vector<double> hsum(ga + gb);
   CUDA_TRY(cudaMemcpyAsync(&hs, dst, sizeof hs, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaMemcpyAsync(hsum.data(), dsum, 8ull * (ga + gb), cudaMemcpyDeviceToHost, ctx.st));
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  // rigorous upper bounds of sum|a_i| and sum|b_j|: device partials are rounded
+  // up; the host sum gets the recursive-summation error margin on top
+  double sa = 0, sb = 0;
+  for (int k = 0; k < ga; ++k) sa += hsum[k];
+  for (int k = 0; k < gb; ++k) sb += hsum[ga + k];
+  sa *= 1.0 + 4.0 * (ga + gb + 2) * 1.1102230246251565e-16;
+  sb *= 1.0 + 4.0 * (ga + gb + 2) * 1.1102230246251565e-16;
+  pb.nonneg = !(hs.negative[0] || hs.negative[1]);
   if (hs.unsorted[0] || hs.unsorted[1])
     return fail(PGPU_EINVAL, "operand exponents are not strictly ascending packed words");
   // exponent fit (core.py:365-385): field sums must stay within the caps
@@ -501,10 +515,21 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
     }
     (void)w;
   }
-  // exact coefficient width: |c| <= min(na,nb) * max|a| * max|b|
+  // exact coefficient width.  |c_k| <= sum over its pairs |a_i||b_j|, which is
+  // <= min(na,nb)*max|a|*max|b| and <= min(sum|a|*max|b|, max|a|*sum|b|).
   pb.nl = 0;
   if (o.coef_kind != PGPU_F64) {
     int need = (int)hs.cbits[0] + (int)hs.cbits[1] + bitlen64(std::min(pb.na, pb.nb)) + 1;
+    double ma, mb;
+    memcpy(&ma, &hs.maxmag[0], 8);
+    memcpy(&mb, &hs.maxmag[1], 8);
+    const double rel = 1.0 + 4.0 * 1.1102230246251565e-16;  // the products below round once
+    double bound = std::min(sa * mb, ma * sb) * rel;
+    if (bound > 0 && std::isfinite(bound)) {
+      int ex;
+      frexp(bound, &ex);  // bound < 2^ex
+      need = std::min(need, ex + 1);
+    }
     pb.need_bits = need;
     int nl = (need + 63) / 64;
     if (nl < 1) nl = 1;
@@ -534,7 +559,7 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   pb.k32 = pos <= 32;
   size_t ksz = pb.k32 ? 4 : 8;
   TRY(ctx.ar->alloc((uint8_t**)&pb.ak, ksz * pb.na));
-  TRY(ctx.ar->alloc((uint8_t**)&pb.bk, ksz * pb.nb));
+  TRY(ctx.ar->alloc((uint8_t**)&pb.bk, ksz * (pb.nb + 128)));  // padded for unrolled loads
   if (pb.k32) {
     k_compact<uint32_t><<<ga, 256, 0, ctx.st>>>(pb.aexp, pb.na, P, (uint32_t*)pb.ak);
     k_compact<uint32_t><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.nb, P, (uint32_t*)pb.bk);

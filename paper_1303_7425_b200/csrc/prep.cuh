@@ -18,6 +18,8 @@ struct OperandStats {
   unsigned long long fmax[2][kMaxFields];
   unsigned int cbits[2];
   unsigned int unsorted[2];
+  unsigned int negative[2];
+  unsigned long long maxmag[2];  // bits of an upper bound (double) of max |c|
 };
 
 __device__ __forceinline__ int bitlen_u64(uint64_t x) { return x ? 64 - __clzll((long long)x) : 0; }
@@ -25,17 +27,20 @@ __device__ __forceinline__ int bitlen_u64(uint64_t x) { return x ? 64 - __clzll(
 template <int CK>
 __global__ void __launch_bounds__(256)
 k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_t n, KeyPlan P,
-        OperandStats* st, int side) {
+        OperandStats* st, int side, double* __restrict__ bsum) {
   const int nf = P.nf;
   __shared__ unsigned long long smax[kMaxFields];
-  __shared__ unsigned int sbits, sunsorted;
+  __shared__ double ssum[32];
+  __shared__ unsigned int sbits, sunsorted, sneg;
   if (threadIdx.x < kMaxFields) smax[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { sbits = 0; sunsorted = 0; }
+  if (threadIdx.x == 0) { sbits = 0; sunsorted = 0; sneg = 0; }
   __syncthreads();
   unsigned long long lmax[kMaxFields];
 #pragma unroll
   for (int f = 0; f < kMaxFields; ++f) lmax[f] = 0;
-  unsigned int lbits = 0, lbad = 0;
+  unsigned int lbits = 0, lbad = 0, lneg = 0;
+  double lsum = 0.0;  // upper bound of sum |c| (rounded up)
+  double lmag = 0.0;  // upper bound of max |c|
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
        i += (int64_t)gridDim.x * blockDim.x) {
     uint64_t e = exps[i];
@@ -49,12 +54,16 @@ k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_
       }
     if constexpr (CK == 1) {
       int64_t c = reinterpret_cast<const int64_t*>(coef)[i];
+      if (c < 0) lneg = 1;
       uint64_t mag = c < 0 ? (uint64_t)(-(c + 1)) + 1 : (uint64_t)c;
       int b = bitlen_u64(mag);
       lbits = b > (int)lbits ? b : lbits;
+      lsum = __dadd_ru(lsum, __ull2double_ru(mag));
+      lmag = fmax(lmag, __ull2double_ru(mag));
     } else if constexpr (CK == 2) {
       const uint64_t* p = reinterpret_cast<const uint64_t*>(coef) + 2 * i;
       uint64_t lo = p[0], hi = p[1];
+      if ((int64_t)hi < 0) lneg = 1;
       if ((int64_t)hi < 0) {  // magnitude of a negative 128-bit value
         lo = ~lo; hi = ~hi;
         lo += 1;
@@ -62,6 +71,10 @@ k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_
       }
       int b = hi ? 64 + bitlen_u64(hi) : bitlen_u64(lo);
       lbits = b > (int)lbits ? b : lbits;
+      double m = __dadd_ru(__dmul_ru(__ull2double_ru(hi), 18446744073709551616.0),
+                           __ull2double_ru(lo));
+      lsum = __dadd_ru(lsum, m);
+      lmag = fmax(lmag, m);
     }
   }
 #pragma unroll
@@ -69,11 +82,23 @@ k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_
     if (f < nf && lmax[f]) atomicMax(&smax[f], lmax[f]);
   if (lbits) atomicMax(&sbits, lbits);
   if (lbad) sunsorted = 1;
+  if (lneg) sneg = 1;
+  // block sum of the per-thread upper bounds, rounded up
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) lsum = __dadd_ru(lsum, __shfl_xor_sync(0xffffffffu, lsum, d));
+  if ((threadIdx.x & 31) == 0) ssum[threadIdx.x >> 5] = lsum;
   __syncthreads();
+  if (lmag > 0.0) atomicMax(&st->maxmag[side], (unsigned long long)__double_as_longlong(lmag));
+  if (threadIdx.x == 0) {
+    double t = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t = __dadd_ru(t, ssum[q]);
+    bsum[blockIdx.x] = t;
+  }
   if (threadIdx.x < nf && smax[threadIdx.x]) atomicMax(&st->fmax[side][threadIdx.x], smax[threadIdx.x]);
   if (threadIdx.x == 0) {
     if (sbits) atomicMax(&st->cbits[side], sbits);
     if (sunsorted) st->unsorted[side] = 1;
+    if (sneg) st->negative[side] = 1;
   }
 }
 
