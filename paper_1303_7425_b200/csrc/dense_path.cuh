@@ -132,7 +132,7 @@ constexpr int kUnroll = 2;           // independent columns per lane per step
 // else as NW word planes.  D = terms per interval.
 template <int NW, int CB>
 struct Geo {
-  static constexpr int NP = CB ? 4 : NW;                 // u32 planes
+  static constexpr int NP = CB ? 4 : NW;                 // u32 planes (4 = two u64 planes)
   static constexpr uint32_t D =
       (uint32_t)(kAccBytes / (kNumWarps * (NP * 4 + CB))) / 32 * 32 - 32;
   static constexpr uint32_t DP = D + 32;                 // + one pad slot per lane
@@ -344,7 +344,17 @@ k_numeric(NumArgs A) {
           const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
           const uint64_t lo = a0 * b0;
           if constexpr (CB) {
-            add_unsigned128<STRIDE>(my + slot[u], myc + slot[u], lo, __umul64hi(a0, b0));
+            // planes 0-1 hold the low u64, planes 2-3 the high u64 of each term
+            uint64_t* p64 = reinterpret_cast<uint64_t*>(acc);
+            const uint32_t e = w * DP + slot[u];
+            uint64_t vlo = p64[e], vhi = p64[STRIDE + e];
+            const uint64_t hi = __umul64hi(a0, b0);
+            uint32_t cy;
+            asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u32 %2, 0, 0;"
+                : "+l"(vlo), "+l"(vhi), "=r"(cy) : "l"(lo), "l"(hi));
+            p64[e] = vlo;
+            p64[STRIDE + e] = vhi;
+            if (cy) cbyte[e] += 1;
           } else {
             uint32_t p[NW];
             const uint64_t hi = __umul64hi(a0, b0);
@@ -431,16 +441,24 @@ k_numeric(NumArgs A) {
           reinterpret_cast<double*>(A.partial)[((uint64_t)t * A.R + r) * D + sl] = v;
         }
       } else {
+        auto word_of = [&](int k, uint32_t e) -> uint32_t {
+          if constexpr (CB) {
+            const uint64_t* p64 = reinterpret_cast<const uint64_t*>(acc);
+            if (k < 2) return (uint32_t)(p64[e] >> (32 * k));
+            if (k < 4) return (uint32_t)(p64[STRIDE + e] >> (32 * (k - 2)));
+            return k == 4 ? (uint32_t)cbyte[e] : 0u;
+          } else {
+            return k < NP ? acc[k * STRIDE + e] : 0u;
+          }
+        };
         uint32_t v[NW];
 #pragma unroll
-        for (int k = 0; k < NW; ++k)
-          v[k] = k < NP ? acc[k * STRIDE + sl] : (k == 4 && CB ? (uint32_t)cbyte[sl] : 0u);
+        for (int k = 0; k < NW; ++k) v[k] = word_of(k, sl);
 #pragma unroll
         for (int q = 1; q < kNumWarps; ++q) {
           uint32_t pw[NW];
 #pragma unroll
-          for (int k = 0; k < NW; ++k)
-            pw[k] = k < NP ? acc[k * STRIDE + q * DP + sl] : (k == 4 && CB ? (uint32_t)cbyte[q * DP + sl] : 0u);
+          for (int k = 0; k < NW; ++k) pw[k] = word_of(k, q * DP + sl);
           uint64_t cy = 0;
 #pragma unroll
           for (int k = 0; k < NW; ++k) {

@@ -1,0 +1,12 @@
+#!/bin/bash
+# Full evidence pass: bench (all legs), reference arm, launch list, ncu of the top kernel.
+cd "$(dirname "$0")/.."
+mkdir -p gpurun_out
+timeout 900 python bench.py --steps 10 --warmup 3 > gpurun_out/bench_full.log 2>&1; echo "bench rc=$?" >> gpurun_out/bench_full.log
+timeout 600 python bench.py --impl reference --steps 3 --warmup 1 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?" >> gpurun_out/bench_ref.log
+for C in fateman20 mp12; do
+  timeout 600 python bench.py --config $C --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$C.log 2>&1
+done
+KREGEX=k_numeric bash tools/gpu_prof.sh > gpurun_out/prof.log 2>&1
+nproc > gpurun_out/nproc.txt; lscpu | head -20 > gpurun_out/lscpu.txt
+tail -c 2500 gpurun_out/bench_full.log; tail -c 800 gpurun_out/bench_ref.log
