@@ -59,6 +59,7 @@ def parse():
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-flush", action="store_true", help="diagnostic only: no L2 flush between steps")
     return ap.parse_args()
 
 
@@ -256,7 +257,8 @@ def main():
     launches = 0
     last = None
     for _ in range(args.steps):
-        flush.zero_()  # evict L2 between timed steps
+        if not args.no_flush:
+            flush.zero_()  # evict L2 between timed steps
         e0 = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
@@ -336,7 +338,7 @@ def main():
                           "result_terms": n_out, "path": path_used, "result_limbs": nl,
                           "parallelism": f"partition_by_ops x{world}" if world > 1 else "1 GPU",
                           "l2": f"flushed ({args.flush_mib} MiB write) between timed steps",
-                          "plan_ms": plan_ms},
+                          "plan_ms": plan_ms, "step_ms": [round(x, 3) for x in times]},
                "roofline": roof, "gpu_launches": launches, "clocks": ck}
 
     # e2e through the C ABI with pinned host buffers (N=1 only)

@@ -30,6 +30,9 @@
 //                             exponent.
 #pragma once
 #include <type_traits>
+#ifndef PGPU_NUM_WARPS
+#define PGPU_NUM_WARPS 16
+#endif
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -119,7 +122,7 @@ __device__ __forceinline__ uint64_t interval_bound(const KT* okey, uint32_t t, u
   return t < T ? (uint64_t)okey[(uint64_t)t * D] : R1;
 }
 
-constexpr int kNumWarps = 8;
+constexpr int kNumWarps = PGPU_NUM_WARPS;
 constexpr int kNumThreads = kNumWarps * 32;
 constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot table
 constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
@@ -250,6 +253,7 @@ k_numeric(NumArgs A) {
   constexpr uint32_t STRIDE = G::stride;
   constexpr int NP = G::NP;
   extern __shared__ __align__(16) uint32_t smem_u32[];
+  __shared__ uint32_t row_ctr;
   uint32_t* acc = smem_u32;                                        // [NP][W][D]
   uint8_t* cbyte = reinterpret_cast<uint8_t*>(acc + NP * STRIDE);  // [W][D] (CB)
   uint16_t* tbl = reinterpret_cast<uint16_t*>(reinterpret_cast<uint8_t*>(smem_u32) + G::tbl_off);
@@ -290,6 +294,7 @@ k_numeric(NumArgs A) {
     const uint32_t base = t * D;
     const uint32_t dcount = min(D, A.nout - base);
     const bool use_tbl = (Khi - Klo) <= kTbl;
+    if (threadIdx.x == 0) row_ctr = 0;
     for (uint32_t k = threadIdx.x; k < G::tbl_off / 4; k += blockDim.x) acc[k] = 0;
     if (use_tbl) {
       const uint64_t w0 = (Klo - A.R0) >> 5, w1 = (Khi - 1 - A.R0) >> 5;
@@ -310,32 +315,59 @@ k_numeric(NumArgs A) {
     uint8_t* myc = cbyte + w * DP;
     // one step: kUnroll columns per lane of row (akr, a0/ad) from cursor c; invalid
     // lanes add into their private pad slot so the step has no divergent branch
+    const uint64_t span_t = Khi - 1 - Klo;
     auto step = [&](const KT akr, const uint64_t a0, const double ad, const uint32_t ri,
                     const uint32_t c, auto tbl_mode) -> uint32_t {
       constexpr bool TBL = decltype(tbl_mode)::value;
+      const KT* __restrict__ bkr = bk + c + lane;  // row-relative: immediate offsets per u
       uint32_t nv = 0;
       uint32_t slot[kUnroll];
-      uint32_t jj[kUnroll];
       bool okk[kUnroll];
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t j = c + lane + 32 * u;
-        const KT key = (KT)(akr + bk[j]);  // bk is padded: the load is in bounds
-        const bool ok = j < nb && key <= kmax;
+        const KT key = (KT)(akr + bkr[32 * u]);  // bk is padded: the load is in bounds
+        const uint64_t dk = (uint64_t)key - Klo;  // wraps for keys below Klo
+        const bool ok = j < nb && (uint64_t)key >= Klo && dk <= span_t;
+        const uint32_t off = (uint32_t)dk;
         nv += __popc(__ballot_sync(0xffffffffu, ok));
         uint32_t sl;
         if constexpr (TBL) {
-          sl = tbl[ok ? (uint32_t)(key - (KT)Klo) : 0u];
+          sl = tbl[min(off, kTbl - 1)];
         } else {
           sl = ok ? rank_of<KT>((uint64_t)key - A.R0, A.bits, A.prefix) - base : 0u;
         }
         slot[u] = ok ? sl : D + lane;
-        jj[u] = ok ? j : 0u;
         okk[u] = ok;
+      }
+      if constexpr (MODE == 1 && CB) {
+        const long long* __restrict__ bcr = reinterpret_cast<const long long*>(A.bc) + c + lane;
+        const uint32_t al = (uint32_t)a0, ah = (uint32_t)(a0 >> 32);
+        uint64_t* p64 = reinterpret_cast<uint64_t*>(acc) + 2 * w * DP;
+#pragma unroll
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint64_t b0 = okk[u] ? (uint64_t)__ldg(bcr + 32 * u) : 0ull;
+          const uint32_t bl = (uint32_t)b0, bh = (uint32_t)(b0 >> 32);
+          // 64x64 -> 128 from four 32x32 -> 64 partial products
+          const uint64_t t0 = (uint64_t)al * bl;
+          const uint64_t t1 = (uint64_t)al * bh + (t0 >> 32);
+          const uint64_t t2 = (uint64_t)ah * bl + (uint32_t)t1;
+          const uint64_t t3 = (uint64_t)ah * bh + (t1 >> 32) + (t2 >> 32);
+          const uint64_t lo = (t2 << 32) | (uint32_t)t0;
+          // one 16-byte element {lo, hi} per (warp, term): a single LDS.128/STS.128
+          ulonglong2* e = reinterpret_cast<ulonglong2*>(p64) + slot[u];
+          ulonglong2 v = *e;
+          uint32_t cy;
+          asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u32 %2, 0, 0;"
+              : "+l"(v.x), "+l"(v.y), "=r"(cy) : "l"(lo), "l"(t3));
+          *e = v;
+          if (cy) cbyte[w * DP + slot[u]] += 1;
+        }
+        return nv;
       }
 #pragma unroll
       for (int u = 0; u < kUnroll; ++u) {
-        const uint32_t j = jj[u];
+        const uint32_t j = okk[u] ? c + lane + 32 * u : 0u;
         if constexpr (MODE == 0) {
           double* d = reinterpret_cast<double*>(acc) + w * DP + slot[u];
           const double bv = okk[u] ? __ldg(reinterpret_cast<const double*>(A.bc) + j) : 0.0;
@@ -343,26 +375,12 @@ k_numeric(NumArgs A) {
         } else if constexpr (MODE == 1) {
           const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
           const uint64_t lo = a0 * b0;
-          if constexpr (CB) {
-            // planes 0-1 hold the low u64, planes 2-3 the high u64 of each term
-            uint64_t* p64 = reinterpret_cast<uint64_t*>(acc);
-            const uint32_t e = w * DP + slot[u];
-            uint64_t vlo = p64[e], vhi = p64[STRIDE + e];
-            const uint64_t hi = __umul64hi(a0, b0);
-            uint32_t cy;
-            asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u32 %2, 0, 0;"
-                : "+l"(vlo), "+l"(vhi), "=r"(cy) : "l"(lo), "l"(hi));
-            p64[e] = vlo;
-            p64[STRIDE + e] = vhi;
-            if (cy) cbyte[e] += 1;
-          } else {
-            uint32_t p[NW];
-            const uint64_t hi = __umul64hi(a0, b0);
-            const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
+          uint32_t p[NW];
+          const uint64_t hi = __umul64hi(a0, b0);
+          const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
 #pragma unroll
-            for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : 0u;
-            add_words<NW, STRIDE>(my + slot[u], p);
-          }
+          for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : 0u;
+          add_words<NW, STRIDE>(my + slot[u], p);
         } else if constexpr (MODE == 2) {
           const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
           const uint64_t lo = a0 * b0;
@@ -387,7 +405,12 @@ k_numeric(NumArgs A) {
       return nv;
     };
     auto rows = [&](auto tbl_mode) {
-      for (uint32_t g = rb0 + w * 32; g < rb1; g += kNumWarps * 32) {
+      // warps claim 32-row groups dynamically (one shared counter per interval)
+      for (;;) {
+        uint32_t g = 0;
+        if (lane == 0) g = atomicAdd(&row_ctr, 32u);
+        g = rb0 + __shfl_sync(0xffffffffu, g, 0);
+        if (g >= rb1) break;
         const uint32_t i = g + lane;
         const bool rowok = i < rb1;
         uint32_t ci = rowok ? cur[i] : 0u;
@@ -443,9 +466,9 @@ k_numeric(NumArgs A) {
       } else {
         auto word_of = [&](int k, uint32_t e) -> uint32_t {
           if constexpr (CB) {
-            const uint64_t* p64 = reinterpret_cast<const uint64_t*>(acc);
-            if (k < 2) return (uint32_t)(p64[e] >> (32 * k));
-            if (k < 4) return (uint32_t)(p64[STRIDE + e] >> (32 * (k - 2)));
+            const uint64_t* p64 = reinterpret_cast<const uint64_t*>(acc);  // [W][DP]{lo,hi}
+            if (k < 2) return (uint32_t)(p64[2 * e] >> (32 * k));
+            if (k < 4) return (uint32_t)(p64[2 * e + 1] >> (32 * (k - 2)));
             return k == 4 ? (uint32_t)cbyte[e] : 0u;
           } else {
             return k < NP ? acc[k * STRIDE + e] : 0u;

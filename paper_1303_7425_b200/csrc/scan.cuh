@@ -3,20 +3,25 @@
 // Reduce-then-scan over G contiguous block ranges: pass 1 sums each range,
 // a single block scans the G partial sums, pass 2 rescans each range with its
 // carry-in and hands (index, exclusive prefix, value) to an output functor.
-// Used for row offsets, run-length heads, and zero-coefficient compaction.
+// Each thread owns kScanIpt consecutive items of a tile (sequential inside the
+// thread, one block scan per tile).  Used for row offsets, the sumset rank
+// words, run-length heads and zero-coefficient compaction.
 #pragma once
 #include "common.cuh"
 
 namespace pgpu {
 
 constexpr int kScanThreads = 256;
+constexpr int kScanIpt = 8;
+constexpr int kScanTile = kScanThreads * kScanIpt;
+constexpr int kMaxScanBlocks = 2048;
 
 template <typename T, typename Gen>
 __global__ void __launch_bounds__(kScanThreads)
 k_range_reduce(uint64_t n, uint64_t per, Gen gen, T* part) {
   __shared__ T sh[33];
-  uint64_t beg = (uint64_t)blockIdx.x * per;
-  uint64_t end = beg + per < n ? beg + per : n;
+  const uint64_t beg = (uint64_t)blockIdx.x * per;
+  const uint64_t end = beg + per < n ? beg + per : n;
   T s = 0;
   for (uint64_t i = beg + threadIdx.x; i < end; i += blockDim.x) s += gen(i);
   s = warp_sum(s);
@@ -49,32 +54,38 @@ template <typename T, typename Gen, typename Out>
 __global__ void __launch_bounds__(kScanThreads)
 k_range_scan(uint64_t n, uint64_t per, Gen gen, Out out, const T* part) {
   __shared__ T sh[33];
-  uint64_t beg = (uint64_t)blockIdx.x * per;
-  uint64_t end = beg + per < n ? beg + per : n;
+  const uint64_t beg = (uint64_t)blockIdx.x * per;
+  const uint64_t end = beg + per < n ? beg + per : n;
   T carry = part[blockIdx.x];
-  for (uint64_t base = beg; base < end; base += blockDim.x) {
-    uint64_t i = base + threadIdx.x;
-    T v = i < end ? gen(i) : T(0);
+  for (uint64_t base = beg; base < end; base += kScanTile) {
+    const uint64_t i0 = base + (uint64_t)threadIdx.x * kScanIpt;
+    T v[kScanIpt];
+    T s = 0;
+#pragma unroll
+    for (int k = 0; k < kScanIpt; ++k) {
+      v[k] = (i0 + k < end) ? gen(i0 + k) : T(0);
+      s += v[k];
+    }
     T tot;
-    T ex = block_excl_scan(v, sh, &tot);
-    if (i < end) out(i, carry + ex, v);
+    T ex = block_excl_scan(s, sh, &tot) + carry;
+#pragma unroll
+    for (int k = 0; k < kScanIpt; ++k) {
+      if (i0 + k < end) out(i0 + k, ex, v[k]);
+      ex += v[k];
+    }
     carry += tot;
   }
 }
 
-// Host driver.  `part` must hold >= G+1 elements (G <= kMaxScanBlocks).
-// Returns the number of kernel launches (3).  The total lands in part[G].
-constexpr int kMaxScanBlocks = 2048;
-
+// Host driver.  `part` must hold >= kMaxScanBlocks+1 elements.
+// Returns the number of kernel launches (3).  The total lands in part[*g_out].
 template <typename T, typename Gen, typename Out>
 int device_scan(uint64_t n, Gen gen, Out out, T* part, int* g_out, cudaStream_t st) {
-  int g = (int)((n + 65535) / 65536);
-  if (g < 1) g = 1;
-  if (g > kMaxScanBlocks) g = kMaxScanBlocks;
-  uint64_t per = (n + g - 1) / g;
-  per = (per + kScanThreads - 1) / kScanThreads * kScanThreads;
-  if (per == 0) per = kScanThreads;
-  g = (int)((n + per - 1) / per);
+  // ~4 tiles per block, at most kMaxScanBlocks blocks
+  uint64_t per = (uint64_t)kScanTile * 4;
+  if ((n + per - 1) / per > (uint64_t)kMaxScanBlocks) per = (n + kMaxScanBlocks - 1) / kMaxScanBlocks;
+  per = (per + kScanTile - 1) / kScanTile * kScanTile;
+  int g = (int)((n + per - 1) / per);
   if (g < 1) g = 1;
   k_range_reduce<T><<<g, kScanThreads, 0, st>>>(n, per, gen, part);
   k_part_scan<T><<<1, 1024, 0, st>>>(part, g);
