@@ -39,29 +39,70 @@
 namespace pgpu {
 
 // ---- D1 ---------------------------------------------------------------------
-constexpr int kSymRows = 64;     // rows per CTA tile
-constexpr int kSymCols = 4096;   // columns per CTA tile (B keys staged in smem)
+// Tiles of kSymRows x kSymCols pairs.  A tile's keys lie in
+// [ak[r0]+bk[c0], ak[r1-1]+bk[c1-1]]; when that window fits kSymWin bytes the
+// tile first marks a shared-memory bytemap (deduplicating the ~16x repeated
+// keys of dense operands) and then writes only the marked bytes to the global
+// bytemap.  Wider tiles store straight to global memory.  Stores are
+// idempotent byte writes of 1: no atomics, independent of order.
+constexpr int kSymRows = 64;
+constexpr int kSymCols = 256;
+constexpr uint32_t kSymWin = 65536;
 
 template <typename KT>
 __global__ void __launch_bounds__(256)
 k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
            const uint32_t* __restrict__ rhi, uint32_t na, uint32_t nb, uint64_t R0,
            uint8_t* __restrict__ bytemap) {
+  extern __shared__ __align__(16) uint8_t win[];  // kSymWin bytes
   __shared__ KT sb[kSymCols];
-  const uint32_t c0 = blockIdx.x * kSymCols;
-  const uint32_t c1 = min(c0 + kSymCols, nb);
-  const uint32_t r0 = blockIdx.y * kSymRows;
-  const uint32_t r1 = min(r0 + kSymRows, na);
-  // rows' column ranges shrink leftwards with i: the tile is empty unless
-  // [rlo[r1-1], rhi[r0]) meets [c0, c1)
-  if (rhi[r0] <= c0 || rlo[r1 - 1] >= c1) return;
-  for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) sb[c - c0] = bk[c];
-  __syncthreads();
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (uint32_t i = r0 + w; i < r1; i += blockDim.x >> 5) {
-    uint32_t lo = max(rlo[i], c0), hi = min(rhi[i], c1);
-    uint64_t a = (uint64_t)ak[i] - R0;
-    for (uint32_t j = lo + lane; j < hi; j += 32) bytemap[a + (uint64_t)sb[j - c0]] = 1;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  const uint32_t ntr = (na + kSymRows - 1) / kSymRows, ntc = (nb + kSymCols - 1) / kSymCols;
+  const uint64_t ntiles = (uint64_t)ntr * ntc;
+  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+    const uint32_t tr = (uint32_t)(tile % ntr), tc = (uint32_t)(tile / ntr);
+    const uint32_t r0 = tr * kSymRows, r1 = min(r0 + kSymRows, na);
+    const uint32_t c0 = tc * kSymCols, c1 = min(c0 + kSymCols, nb);
+    // rows' column ranges shrink leftwards with i: the tile is empty unless
+    // [rlo[r1-1], rhi[r0]) meets [c0, c1)
+    if (rhi[r0] <= c0 || rlo[r1 - 1] >= c1) continue;
+    // window aligned to 16 keys (relative to R0) so the flush can OR whole words
+    const uint64_t wlo = R0 + (((uint64_t)ak[r0] + (uint64_t)bk[c0] - R0) & ~15ull);
+    const uint64_t whi = (uint64_t)ak[r1 - 1] + (uint64_t)bk[c1 - 1];
+    const bool local = whi - wlo < kSymWin;
+    const uint32_t wn = local ? (uint32_t)(whi - wlo + 1) : 0u;
+    for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) sb[c - c0] = bk[c];
+    if (local)
+      for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x)
+        reinterpret_cast<uint4*>(win)[q] = make_uint4(0, 0, 0, 0);
+    __syncthreads();
+    for (uint32_t i = r0 + w; i < r1; i += nw) {
+      const uint32_t lo = max(rlo[i], c0), hi = min(rhi[i], c1);
+      const uint64_t ai = ak[i];
+      if (local) {
+        const uint32_t ao = (uint32_t)(ai + (uint64_t)bk[c0] - wlo);  // offset of column c0
+        const uint64_t b0 = (uint64_t)sb[0];
+        for (uint32_t j = lo + lane; j < hi; j += 32)
+          win[ao + (uint32_t)((uint64_t)sb[j - c0] - b0)] = 1;
+      } else {
+        const uint64_t a = ai - R0;
+        for (uint32_t j = lo + lane; j < hi; j += 32) bytemap[a + (uint64_t)sb[j - c0]] = 1;
+      }
+    }
+    __syncthreads();
+    if (local) {
+      // OR the marked words into the global bytemap (other tiles set other bytes
+      // of the same words concurrently, so whole-word plain stores are not safe)
+      unsigned int* dst = reinterpret_cast<unsigned int*>(bytemap + (wlo - R0));
+      for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x) {
+        const uint4 v = reinterpret_cast<const uint4*>(win)[q];
+        if (v.x) atomicOr(dst + 4 * q, v.x);
+        if (v.y) atomicOr(dst + 4 * q + 1, v.y);
+        if (v.z) atomicOr(dst + 4 * q + 2, v.z);
+        if (v.w) atomicOr(dst + 4 * q + 3, v.w);
+      }
+    }
+    __syncthreads();
   }
 }
 

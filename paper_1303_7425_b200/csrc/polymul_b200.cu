@@ -67,10 +67,15 @@ struct Status {
 
 #define LAUNCHED(k) (ctx.launches += (k))
 
-// Per-device state: library stream and a retained stream-ordered pool.
+// Per-device state: library stream, a retained stream-ordered pool, and a
+// persistent scratch workspace (bump-allocated per call, grown between calls).
 struct DeviceState {
   bool init = false;
   cudaStream_t stream = nullptr;
+  uint8_t* ws = nullptr;
+  size_t ws_cap = 0;
+  size_t ws_want = 0;  // high-water mark requested by previous calls
+  std::mutex mu;       // one product per device at a time uses the workspace
 };
 std::mutex g_mu;
 DeviceState g_dev[64];
@@ -91,17 +96,40 @@ int device_setup(int dev, cudaStream_t* st) {
   return PGPU_OK;
 }
 
-// Stream-ordered scratch; everything not handed to the caller is freed at scope exit.
+// Scratch allocator.  Requests are bump-allocated from the device workspace;
+// when it is too small the request falls back to cudaMallocAsync and the
+// workspace is regrown after the call.  Memory handed to the caller always
+// comes from cudaMallocAsync (it outlives the call).
 struct Arena {
   cudaStream_t st;
-  std::vector<void*> ptrs;
-  explicit Arena(cudaStream_t s) : st(s) {}
+  DeviceState* dev = nullptr;
+  size_t used = 0;
+  size_t requested = 0;
+  std::vector<void*> ptrs;  // cudaMallocAsync allocations owned by the arena
+  explicit Arena(cudaStream_t s, DeviceState* d = nullptr) : st(s), dev(d) {}
   ~Arena() {
     for (void* p : ptrs) cudaFreeAsync(p, st);
+    if (dev && requested > dev->ws_want) dev->ws_want = requested;
   }
   template <typename T>
   int alloc(T** p, size_t count) {
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    bytes = (bytes + 255) & ~size_t(255);
+    requested += bytes;
+    if (dev && dev->ws && used + bytes <= dev->ws_cap) {
+      *p = reinterpret_cast<T*>(dev->ws + used);
+      used += bytes;
+      return PGPU_OK;
+    }
+    return alloc_fresh(p, bytes);
+  }
+  template <typename T>
+  int alloc_out(T** p, size_t count) {  // caller-owned result buffer
+    size_t bytes = std::max<size_t>(count * sizeof(T), 16);
+    return alloc_fresh(p, bytes);
+  }
+  template <typename T>
+  int alloc_fresh(T** p, size_t bytes) {
     cudaError_t e = cudaMallocAsync((void**)p, bytes, st);
     if (e != cudaSuccess) {
       cudaGetLastError();
@@ -111,10 +139,32 @@ struct Arena {
     ptrs.push_back((void*)*p);
     return PGPU_OK;
   }
+  bool owns(void* p) const { return std::find(ptrs.begin(), ptrs.end(), p) != ptrs.end(); }
   void release(void* p) {  // ownership moves to the caller
     ptrs.erase(std::remove(ptrs.begin(), ptrs.end(), p), ptrs.end());
   }
 };
+
+// Grow the workspace to the last call's high-water mark (between calls only).
+int grow_workspace(DeviceState& d, cudaStream_t st) {
+  if (d.ws_want <= d.ws_cap) return PGPU_OK;
+  size_t freeb = 0, totb = 0;
+  CUDA_TRY(cudaStreamSynchronize(st));
+  if (d.ws) CUDA_TRY(cudaFree(d.ws));
+  d.ws = nullptr;
+  d.ws_cap = 0;
+  CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
+  size_t want = d.ws_want + d.ws_want / 4;
+  if (want > freeb / 2) want = d.ws_want <= freeb / 2 ? d.ws_want : 0;  // keep room for the pool
+  if (want == 0) return PGPU_OK;
+  if (cudaMalloc((void**)&d.ws, want) != cudaSuccess) {
+    cudaGetLastError();
+    d.ws = nullptr;
+    return PGPU_OK;  // fall back to per-call allocations
+  }
+  d.ws_cap = want;
+  return PGPU_OK;
+}
 
 struct Timer {
   bool on = false;
@@ -334,8 +384,8 @@ int sort_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t p
   ctx.tm.mark(3, "reduce");
   // compaction of zero sums
   uint64_t *cexp, *ccoef;
-  TRY(ctx.ar->alloc(&cexp, nseg));
-  TRY(ctx.ar->alloc(&ccoef, (size_t)nseg * nl));
+  TRY(ctx.ar->alloc_out(&cexp, nseg));
+  TRY(ctx.ar->alloc_out(&ccoef, (size_t)nseg * nl));
   LAUNCHED(device_scan<uint32_t>(nseg, FlagGen{snz}, CompactOut{sexp, scoef, nl, cexp, ccoef}, part,
                                  &g, ctx.st));
   uint32_t nnz;
@@ -635,7 +685,10 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   Ctx ctx;
   ctx.st = o.stream ? (cudaStream_t)o.stream : lib_st;
   CUDA_TRY(cudaDeviceGetAttribute(&ctx.sms, cudaDevAttrMultiProcessorCount, o.device));
-  Arena ar(ctx.st);
+  DeviceState& dstate = g_dev[o.device & 63];
+  std::lock_guard<std::mutex> ws_lock(dstate.mu);
+  TRY(grow_workspace(dstate, ctx.st));
+  Arena ar(ctx.st, &dstate);
   ctx.ar = &ar;
   ctx.tm.start(ctx.st, o.timing != 0);
 
@@ -691,12 +744,12 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   out->acc_limbs = nl;
   if (o.outputs_on_device) {
     uint64_t *e, *c;
-    if (slices.size() == 1) {
+    if (slices.size() == 1 && ar.owns(slices[0].exps) && ar.owns(slices[0].coef)) {
       e = slices[0].exps;
       c = slices[0].coef;
     } else {
-      TRY(ar.alloc(&e, n));
-      TRY(ar.alloc(&c, n * nl));
+      TRY(ar.alloc_out(&e, n));
+      TRY(ar.alloc_out(&c, n * nl));
       uint64_t at = 0;
       for (auto& s : slices) {
         CUDA_TRY(cudaMemcpyAsync(e + at, s.exps, s.n * 8, cudaMemcpyDeviceToDevice, ctx.st));
