@@ -18,6 +18,7 @@ F64, I64, I128 = 0, 1, 2
 PATH_AUTO, PATH_DENSE, PATH_SORT = 0, 1, 2
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpolymul_b200.so"
+# PGPU_LIB: load a different build of the same library (kernel-variant experiments)
 
 # Every symbol include/polymul_b200.h declares (checked by the CPU test suite).
 EXPORTS = ("pgpu_default_options", "pgpu_mul", "pgpu_count_below", "pgpu_free_result",
@@ -63,7 +64,8 @@ def load(path: Path | None = None) -> C.CDLL:
     with _lock:
         if _lib is not None:
             return _lib
-        p = Path(path) if path else LIB_PATH
+        import os
+        p = Path(path) if path else Path(os.environ.get("PGPU_LIB", str(LIB_PATH)))
         if not p.exists():
             raise ImportError(
                 f"{p} is missing: build it with `python -m paper_1303_7425_b200.build` "

@@ -47,13 +47,15 @@ def stale() -> bool:
     return any(s.stat().st_mtime > t for s in sources())
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, out: Path | None = None,
+          defines: tuple = ()) -> Path:
+    if out is None and not force and not stale():
         return LIB
     LIBDIR.mkdir(exist_ok=True)
-    tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-I", str(ROOT / "include"), str(CSRC / "polymul_b200.cu"),
-           "-o", str(tmp)]
+    target = Path(out) if out else LIB
+    tmp = target.with_suffix(".so.tmp")
+    cmd = [nvcc(), *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", str(ROOT / "include"),
+           str(CSRC / "polymul_b200.cu"), "-o", str(tmp)]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -61,8 +63,8 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
     if verbose and (res.stdout or res.stderr):
         print(res.stdout, res.stderr, file=sys.stderr)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, target)
+    return target
 
 
 if __name__ == "__main__":

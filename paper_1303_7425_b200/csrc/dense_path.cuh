@@ -30,6 +30,9 @@
 //                             exponent.
 #pragma once
 #include <type_traits>
+#ifndef PGPU_UNROLL
+#define PGPU_UNROLL 1
+#endif
 #ifndef PGPU_NUM_WARPS
 #define PGPU_NUM_WARPS 16
 #endif
@@ -168,7 +171,7 @@ constexpr int kNumThreads = kNumWarps * 32;
 constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot table
 constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
 constexpr size_t kAccBytes = 80 * 1024;
-constexpr int kUnroll = 2;           // independent columns per lane per step
+constexpr int kUnroll = PGPU_UNROLL;           // independent columns per lane per step
 
 // Accumulator geometry.  NW = words of a finished term.  CB = 1: the term is
 // held as 4 word planes plus a one-byte carry counter (nonnegative products

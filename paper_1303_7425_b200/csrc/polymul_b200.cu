@@ -96,6 +96,9 @@ int device_setup(int dev, cudaStream_t* st) {
   return PGPU_OK;
 }
 
+constexpr size_t kWorkspaceMaxItem = 1ull << 30;  // larger buffers bypass the workspace
+constexpr size_t kWorkspaceMax = 16ull << 30;     // workspace never grows beyond this
+
 // Scratch allocator.  Requests are bump-allocated from the device workspace;
 // when it is too small the request falls back to cudaMallocAsync and the
 // workspace is regrown after the call.  Memory handed to the caller always
@@ -106,7 +109,8 @@ struct Arena {
   size_t used = 0;
   size_t requested = 0;
   std::vector<void*> ptrs;  // cudaMallocAsync allocations owned by the arena
-  explicit Arena(cudaStream_t s, DeviceState* d = nullptr) : st(s), dev(d) {}
+  explicit Arena(cudaStream_t s, DeviceState* d = nullptr, size_t base = 0)
+      : st(s), dev(d), used(base), requested(base) {}
   ~Arena() {
     for (void* p : ptrs) cudaFreeAsync(p, st);
     if (dev && requested > dev->ws_want) dev->ws_want = requested;
@@ -115,6 +119,7 @@ struct Arena {
   int alloc(T** p, size_t count) {
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     bytes = (bytes + 255) & ~size_t(255);
+    if (bytes > kWorkspaceMaxItem) return alloc_fresh(p, bytes);  // big batch buffers: pool only
     requested += bytes;
     if (dev && dev->ws && used + bytes <= dev->ws_cap) {
       *p = reinterpret_cast<T*>(dev->ws + used);
@@ -154,7 +159,7 @@ int grow_workspace(DeviceState& d, cudaStream_t st) {
   d.ws = nullptr;
   d.ws_cap = 0;
   CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
-  size_t want = d.ws_want + d.ws_want / 4;
+  size_t want = std::min(d.ws_want + d.ws_want / 4, kWorkspaceMax);
   if (want > freeb / 2) want = d.ws_want <= freeb / 2 ? d.ws_want : 0;  // keep room for the pool
   if (want == 0) return PGPU_OK;
   if (cudaMalloc((void**)&d.ws, want) != cudaSuccess) {
@@ -321,7 +326,25 @@ int radix_sort(Ctx& ctx, KT** keys, uint64_t** vals, KT* kalt, uint64_t* valt, u
 }
 
 template <typename KT>
+int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
+                    uint64_t pairs, Slice* out);
+
+// One batch: its scratch lives in a batch-scoped arena (returned to the pool
+// before the next batch); only the compacted output is owned by the caller's arena.
+template <typename KT>
 int sort_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t pairs, Slice* out) {
+  Arena* outer = ctx.ar;
+  // nested: small batches bump-allocate above the caller's workspace usage
+  Arena batch(ctx.st, pairs * 48 < (64ull << 20) ? outer->dev : nullptr, outer->used);
+  ctx.ar = &batch;
+  int r = sort_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out);
+  ctx.ar = outer;
+  return r;
+}
+
+template <typename KT>
+int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
+                    uint64_t pairs, Slice* out) {
   out->n = 0;
   if (pairs == 0) return PGPU_OK;
   uint32_t *rlo, *rhi;
@@ -384,8 +407,8 @@ int sort_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t p
   ctx.tm.mark(3, "reduce");
   // compaction of zero sums
   uint64_t *cexp, *ccoef;
-  TRY(ctx.ar->alloc_out(&cexp, nseg));
-  TRY(ctx.ar->alloc_out(&ccoef, (size_t)nseg * nl));
+  TRY(outer->alloc_out(&cexp, nseg));
+  TRY(outer->alloc_out(&ccoef, (size_t)nseg * nl));
   LAUNCHED(device_scan<uint32_t>(nseg, FlagGen{snz}, CompactOut{sexp, scoef, nl, cexp, ccoef}, part,
                                  &g, ctx.st));
   uint32_t nnz;
@@ -489,9 +512,11 @@ template <typename KT>
 int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice>& slices) {
   size_t freeb = 0, totb = 0;
   CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
-  uint64_t bpp = 2 * (sizeof(KT) + 8) + 4 + 8;  // records x2, starts, slack
-  uint64_t cap = (uint64_t)(freeb * 0.80) / bpp;
-  if (cap > 0xfffffff0ull) cap = 0xfffffff0ull;  // 32-bit positions inside a batch
+  // per pair: records x2 (key + i<<32|j), segment starts; the segment outputs
+  // (<= pairs, usually far fewer) and scan scratch fit in the remaining slack
+  uint64_t bpp = 2 * (sizeof(KT) + 8) + 4 + 8;
+  uint64_t cap = (uint64_t)(freeb * 0.55) / bpp;
+  if (cap > (1ull << 31)) cap = 1ull << 31;  // 32-bit positions inside a batch
   const char* env = getenv("PGPU_BATCH_CAP");
   if (env) cap = std::min<uint64_t>(cap, strtoull(env, nullptr, 10));
   std::vector<std::pair<uint64_t, uint64_t>> ranges;

@@ -153,3 +153,29 @@ def test_result_class_follows_operand_class():
     p = mul(a, a)
     assert type(p) is Polynomial
     p.validate()
+
+
+def test_mp25_full_product_term_count():
+    """Full Monagan-Pearce n=25 product on one GPU (batched sort path):
+    312,855,140 terms, left in device memory."""
+    import torch
+    from paper_1303_7425_b200.device import DeviceOperand, mul_on_device
+    d = digests()["mp25_intervals"]
+    f, g = benchpolys.monagan_pearce(25)
+    dev = torch.device("cuda", 0)
+    A, B = DeviceOperand(Operand.from_poly(f), dev), DeviceOperand(Operand.from_poly(g), dev)
+    r = mul_on_device(A, B, f.layout)
+    try:
+        assert r.pairs == d["total_ops"]
+        assert r.n == d["result_terms"]
+    finally:
+        r.free()
+
+
+def test_batched_sort_path_matches_single_batch(monkeypatch):
+    """Force tiny batches: the concatenated batches equal the one-shot product."""
+    f, g = benchpolys.monagan_pearce(6)
+    whole = mul(f, g, MulConfig(path="sort"))
+    monkeypatch.setenv("PGPU_BATCH_CAP", "20000")
+    batched = mul(f, g, MulConfig(path="sort"))
+    assert batched.exps == whole.exps and batched.coeffs == whole.coeffs
