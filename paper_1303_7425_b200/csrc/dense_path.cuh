@@ -59,6 +59,8 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
            uint8_t* __restrict__ bytemap) {
   extern __shared__ __align__(16) uint8_t win[];  // kSymWin bytes
   __shared__ KT sb[kSymCols];
+  __shared__ KT sa[kSymRows];
+  __shared__ uint32_t slo[kSymRows], shi[kSymRows];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t ntr = (na + kSymRows - 1) / kSymRows, ntc = (nb + kSymCols - 1) / kSymCols;
   const uint64_t ntiles = (uint64_t)ntr * ntc;
@@ -75,13 +77,18 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
     const bool local = whi - wlo < kSymWin;
     const uint32_t wn = local ? (uint32_t)(whi - wlo + 1) : 0u;
     for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) sb[c - c0] = bk[c];
+    for (uint32_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
+      sa[i - r0] = ak[i];
+      slo[i - r0] = max(rlo[i], c0);
+      shi[i - r0] = min(rhi[i], c1);
+    }
     if (local)
       for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x)
         reinterpret_cast<uint4*>(win)[q] = make_uint4(0, 0, 0, 0);
     __syncthreads();
     for (uint32_t i = r0 + w; i < r1; i += nw) {
-      const uint32_t lo = max(rlo[i], c0), hi = min(rhi[i], c1);
-      const uint64_t ai = ak[i];
+      const uint32_t lo = slo[i - r0], hi = shi[i - r0];
+      const uint64_t ai = sa[i - r0];
       if (local) {
         const uint32_t ao = (uint32_t)(ai + (uint64_t)bk[c0] - wlo);  // offset of column c0
         const uint64_t b0 = (uint64_t)sb[0];

@@ -863,8 +863,10 @@ int pgpu_count_below(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* 
 void pgpu_free_result(pgpu_result* r) {
   if (!r) return;
   if (r->on_device) {
-    if (r->exps) cudaFree(r->exps);
-    if (r->coeffs) cudaFree(r->coeffs);
+    // stream-ordered free on the legacy default stream: the memory goes back to
+    // the (retained) pool for the next product instead of to the driver
+    if (r->exps) cudaFreeAsync(r->exps, 0);
+    if (r->coeffs) cudaFreeAsync(r->coeffs, 0);
   } else {
     free(r->exps);
     free(r->coeffs);
