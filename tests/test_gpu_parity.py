@@ -179,3 +179,80 @@ def test_batched_sort_path_matches_single_batch(monkeypatch):
     monkeypatch.setenv("PGPU_BATCH_CAP", "20000")
     batched = mul(f, g, MulConfig(path="sort"))
     assert batched.exps == whole.exps and batched.coeffs == whole.coeffs
+
+
+@pytest.mark.parametrize("path", ["dense", "sort"])
+def test_disjoint_ranges_concatenate_to_the_product(path):
+    """The multi-GPU contract: products restricted to consecutive packed ranges
+    [S_k, S_k+1) concatenate to the full product (split.py:5-9)."""
+    f, g = benchpolys.fateman(8)
+    A, B = Operand.from_poly(f), Operand.from_poly(g)
+    full = native_mul(A, B, f.layout, path=path)
+    bounds = select_grid(f, g, GridParams(5)).bounds
+    cuts = [0] + bounds[1:-1:3] + [(1 << 64) - 1]
+    exps, limbs = [], []
+    for lo, hi in zip(cuts, cuts[1:]):
+        r = native_mul(A, B, f.layout, lo=lo, hi=hi, path=path)
+        exps.append(r.exps)
+        limbs.append(r.coef)
+    assert np.array_equal(np.concatenate(exps), full.exps)
+    assert np.array_equal(np.concatenate(limbs), full.coef)
+
+
+def test_dense_float_matches_oracle_within_bound(rng):
+    from oracle import oracle as O
+    from paper_1303_7425_b200.core import Polynomial as P
+    lay = default_layout(("x", "y", "z"))
+    for _ in range(5):
+        a = P(lay, [(rng.uniform(-5, 5), (rng.randint(0, 9), rng.randint(0, 9), rng.randint(0, 9)))
+                    for _ in range(300)], float)
+        b = P(lay, [(rng.uniform(-5, 5), (rng.randint(0, 9), rng.randint(0, 9), rng.randint(0, 9)))
+                    for _ in range(300)], float)
+        got = mul(a, b, MulConfig(path="dense"))
+        want = O.mul(a, b)
+        absa = P._from_sorted(lay, a.exps, [abs(c) for c in a.coeffs], float)
+        absb = P._from_sorted(lay, b.exps, [abs(c) for c in b.coeffs], float)
+        mag = dict(zip(*[O.mul(absa, absb).exps, O.mul(absa, absb).coeffs]))
+        # terms whose reference sum is exactly 0 are dropped by both; tiny
+        # cancellations may survive on one side only, within the bound
+        gd = dict(zip(got.exps, got.coeffs))
+        wd = dict(zip(want.exps, want.coeffs))
+        k = min(a.n, b.n)
+        for e in set(gd) | set(wd):
+            tol = 2 * k * 2.0 ** -53 * mag[e]
+            assert abs(gd.get(e, 0.0) - wd.get(e, 0.0)) <= tol
+
+
+@pytest.mark.parametrize("path", ["dense", "sort"])
+def test_int128_operands_signed(path, rng):
+    """Operands beyond 63 bits (two-limb int128) with mixed signs."""
+    from paper_1303_7425_b200.core import Polynomial as P
+    lay = default_layout(("x", "y"))
+    big = lambda: rng.choice([-1, 1]) * rng.randint(1 << 70, 1 << 90)
+    a = P(lay, [(big(), (rng.randint(0, 20), rng.randint(0, 20))) for _ in range(150)])
+    b = P(lay, [(big(), (rng.randint(0, 20), rng.randint(0, 20))) for _ in range(150)])
+    want = {}
+    for ea, ca in zip(a.exps, a.coeffs):
+        for eb, cb in zip(b.exps, b.coeffs):
+            want[ea + eb] = want.get(ea + eb, 0) + ca * cb
+    got = mul(a, b, MulConfig(path=path))
+    assert got.exps == sorted(e for e, v in want.items() if v)
+    assert got.coeffs == [want[e] for e in got.exps]
+
+
+def test_device_resident_api_and_free():
+    import torch
+    from paper_1303_7425_b200.device import DeviceOperand, mul_on_device
+    from paper_1303_7425_b200.parmul import limbs_to_ints
+    f, g = benchpolys.fateman(6)
+    dev = torch.device("cuda", 0)
+    A, B = DeviceOperand(Operand.from_poly(f), dev), DeviceOperand(Operand.from_poly(g), dev)
+    for _ in range(3):
+        r = mul_on_device(A, B, f.layout, stream=torch.cuda.current_stream().cuda_stream, timing=True)
+        e, c = r.tensors()
+        exps = e.cpu().numpy().view(np.uint64).tolist()
+        co = limbs_to_ints(c.cpu().numpy().view(np.uint64), r.nl)
+        r.free()
+        want = mul(f, g, MulConfig(path="sort"))
+        assert exps == want.exps and co == want.coeffs
+        assert r.launches > 0 and "numeric" in r.phases
