@@ -301,22 +301,36 @@ template <typename KT>
 int radix_sort(Ctx& ctx, KT** keys, uint64_t** vals, KT* kalt, uint64_t* valt, uint64_t n,
                int bits) {
   if (n <= 1 || bits <= 0) return PGPU_OK;
-  int G = (int)std::min<uint64_t>((n + kRsTile - 1) / kRsTile, (uint64_t)ctx.sms * 4);
-  if (G < 1) G = 1;
-  uint64_t per = (n + G - 1) / G;
-  per = (per + kRsTile - 1) / kRsTile * kRsTile;
-  G = (int)((n + per - 1) / per);
-  uint32_t* counts;
-  TRY(ctx.ar->alloc(&counts, (size_t)kRsDigits * G));
+  const int npass = (bits + 7) / 8;
+  if (npass > kRsMaxPasses) return fail(PGPU_EUNSUPPORTED, "sort key wider than 64 bits");
+  const uint64_t ntiles = (n + kRsTile - 1) / kRsTile;
+  unsigned int* ghist;
+  unsigned long long* status;
+  unsigned int* ctr;
+  TRY(ctx.ar->alloc(&ghist, (size_t)kRsMaxPasses * kRsDigits));
+  TRY(ctx.ar->alloc(&status, (size_t)ntiles * kRsDigits));
+  TRY(ctx.ar->alloc(&ctr, npass));
+  CUDA_TRY(cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * kRsMaxPasses * kRsDigits, ctx.st));
+  CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned int) * npass, ctx.st));
+  k_rs_hist_all<KT><<<grid_for((int64_t)((n + kRsThreads - 1) / kRsThreads), 1, ctx.sms * 8),
+                      kRsThreads, 0, ctx.st>>>(*keys, n, npass, ghist);
+  k_rs_hist_scan<<<1, kRsDigits, 0, ctx.st>>>(ghist, npass);
+  LAUNCHED(2);
+  const size_t smem = (sizeof(KT) + 8) * (size_t)kRsTile;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(k_rs_onesweep<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    attr_set = true;
+  }
   KT* kin = *keys;
   uint64_t* vin = *vals;
   KT* kout = kalt;
   uint64_t* vout = valt;
-  for (int shift = 0; shift < bits; shift += 8) {
-    k_rs_hist<KT><<<G, kRsThreads, 0, ctx.st>>>(kin, n, per, shift, G, counts);
-    k_rs_scan<<<1, 1024, 0, ctx.st>>>(counts, kRsDigits * G);
-    k_rs_scatter<KT><<<G, kRsThreads, 0, ctx.st>>>(kin, vin, kout, vout, n, per, shift, G, counts);
-    LAUNCHED(3);
+  for (int p = 0; p < npass; ++p) {
+    CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ntiles * kRsDigits, ctx.st));
+    k_rs_onesweep<KT><<<(unsigned)ntiles, kRsThreads, smem, ctx.st>>>(
+        kin, vin, kout, vout, n, 8 * p, ghist + p * kRsDigits, status, ctr + p);
+    LAUNCHED(1);
     std::swap(kin, kout);
     std::swap(vin, vout);
   }

@@ -42,12 +42,23 @@ k_gen(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __re
   }
 }
 
-// ---- K2: LSD radix sort ----------------------------------------------------
+// ---- K2: LSD radix sort (onesweep) ------------------------------------------
+// One upfront histogram kernel gives every pass's global digit counts (the
+// multiset of keys is the same for all passes).  Each pass is then a single
+// kernel: tiles are claimed in launch order through a counter, rank their
+// items stably with warp ballots (no shared-memory atomics), publish per-digit
+// tile counts and find their exclusive prefix by decoupled look-back over the
+// previous tiles, then scatter through shared memory so that global writes of
+// equal digits are contiguous.
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsIpt = 8;                          // items per thread per tile
-constexpr int kRsTile = kRsThreads * kRsIpt;       // 2048
+constexpr int kRsIpt = 16;                         // items per thread per tile
+constexpr int kRsTile = kRsThreads * kRsIpt;       // 4096
 constexpr int kRsDigits = 256;
+constexpr int kRsMaxPasses = 8;
+constexpr unsigned long long kFlagAgg = 1ull << 62;
+constexpr unsigned long long kFlagPre = 2ull << 62;
+constexpr unsigned long long kValMask = (1ull << 62) - 1;
 
 __device__ __forceinline__ unsigned lanemask_lt() {
   unsigned m;
@@ -67,130 +78,146 @@ __device__ __forceinline__ unsigned digit_peers(unsigned d, unsigned valid) {
   return peers;
 }
 
+// ghist[p][d]: number of keys whose digit p is d, for all passes at once.
 template <typename KT>
 __global__ void __launch_bounds__(kRsThreads)
-k_rs_hist(const KT* __restrict__ keys, uint64_t n, uint64_t per, int shift, int G,
-          uint32_t* __restrict__ counts) {
-  __shared__ uint32_t wh[kRsWarps][kRsDigits];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wh[0][0])[k] = 0;
+k_rs_hist_all(const KT* __restrict__ keys, uint64_t n, int npass, unsigned int* __restrict__ ghist) {
+  __shared__ uint32_t h[kRsMaxPasses][kRsDigits];
+  const int lane = threadIdx.x & 31;
+  for (int k = threadIdx.x; k < kRsMaxPasses * kRsDigits; k += blockDim.x) (&h[0][0])[k] = 0;
   __syncthreads();
-  uint64_t beg = (uint64_t)blockIdx.x * per;
-  uint64_t end = beg + per < n ? beg + per : n;
-  for (uint64_t base = beg; base < end; base += kRsThreads) {
-    uint64_t idx = base + threadIdx.x;
-    bool ok = idx < end;
-    unsigned d = ok ? (unsigned)((uint64_t)keys[idx] >> shift) & 0xffu : 0u;
-    unsigned valid = __ballot_sync(0xffffffffu, ok);
-    unsigned peers = digit_peers(d, valid);
-    if (ok && (peers & lanemask_lt()) == 0) wh[w][d] += __popc(peers);
-    __syncwarp();
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t base = (uint64_t)blockIdx.x * blockDim.x; base < n; base += stride) {
+    const uint64_t idx = base + threadIdx.x;
+    const bool ok = idx < n;
+    const uint64_t k = ok ? (uint64_t)keys[idx] : 0ull;
+    const unsigned valid = __ballot_sync(0xffffffffu, ok);
+    for (int p = 0; p < npass; ++p) {
+      const unsigned d = (unsigned)(k >> (8 * p)) & 0xffu;
+      const unsigned peers = __match_any_sync(0xffffffffu, ok ? d : 0x100u) & valid;
+      // one leader per digit group: shared-memory atomic add per group (few)
+      if (ok && (peers & lanemask_lt()) == 0) atomicAdd(&h[p][d], (uint32_t)__popc(peers));
+    }
   }
   __syncthreads();
-  for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x) {
-    uint32_t s = 0;
-#pragma unroll
-    for (int q = 0; q < kRsWarps; ++q) s += wh[q][d];
-    counts[(uint64_t)d * G + blockIdx.x] = s;
-  }
+  for (int k = threadIdx.x; k < npass * kRsDigits; k += blockDim.x)
+    if ((&h[0][0])[k]) atomicAdd(ghist + k, (&h[0][0])[k]);
 }
 
-// Exclusive scan of counts[256*G] in (digit, block) order, in place.
-__global__ void __launch_bounds__(1024) k_rs_scan(uint32_t* counts, int total) {
+// Exclusive scan of each pass's 256 counts, in place (one block).
+__global__ void __launch_bounds__(kRsDigits) k_rs_hist_scan(unsigned int* ghist, int npass) {
   __shared__ uint32_t sh[33];
-  uint32_t carry = 0;
-  for (int base = 0; base < total; base += blockDim.x) {
-    int i = base + threadIdx.x;
-    uint32_t v = i < total ? counts[i] : 0u;
+  for (int p = 0; p < npass; ++p) {
+    uint32_t v = ghist[p * kRsDigits + threadIdx.x];
     uint32_t tot;
     uint32_t ex = block_excl_scan(v, sh, &tot);
-    if (i < total) counts[i] = carry + ex;
-    carry += tot;
+    ghist[p * kRsDigits + threadIdx.x] = ex;
   }
 }
 
 template <typename KT>
 __global__ void __launch_bounds__(kRsThreads)
-k_rs_scatter(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* __restrict__ kout,
-             uint64_t* __restrict__ vout, uint64_t n, uint64_t per, int shift, int G,
-             const uint32_t* __restrict__ offs) {
+k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* __restrict__ kout,
+              uint64_t* __restrict__ vout, uint64_t n, int shift, const unsigned int* __restrict__ gbase,
+              unsigned long long* status, unsigned int* tile_ctr) {
+  extern __shared__ __align__(16) uint8_t rs_smem[];
+  KT* skey = reinterpret_cast<KT*>(rs_smem);                                   // [kRsTile]
+  uint64_t* sval = reinterpret_cast<uint64_t*>(rs_smem + sizeof(KT) * kRsTile);  // [kRsTile]
   __shared__ uint32_t wcnt[kRsWarps][kRsDigits];
-  __shared__ uint32_t run_off[kRsDigits];
   __shared__ uint32_t tstart[kRsDigits];
   __shared__ uint32_t ttot[kRsDigits];
+  __shared__ unsigned long long gpre[kRsDigits];
   __shared__ uint32_t shs[33];
-  __shared__ KT skey[kRsTile];
-  __shared__ uint64_t sval[kRsTile];
+  __shared__ uint32_t tile_s;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const unsigned lt = lanemask_lt();
-  for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x)
-    run_off[d] = offs[(uint64_t)d * G + blockIdx.x];
-  uint64_t beg = (uint64_t)blockIdx.x * per;
-  uint64_t end = beg + per < n ? beg + per : n;
-  for (uint64_t t0 = beg; t0 < end; t0 += kRsTile) {
-    for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wcnt[0][0])[k] = 0;
-    __syncthreads();
-    KT key[kRsIpt];
-    uint64_t val[kRsIpt];
-    uint32_t rank[kRsIpt];
-    unsigned dig[kRsIpt];
-    // warp w owns tile items [w*256, (w+1)*256): warp-major order is input order
+  if (threadIdx.x == 0) tile_s = atomicAdd(tile_ctr, 1u);
+  for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wcnt[0][0])[k] = 0;
+  __syncthreads();
+  const uint32_t t = tile_s;
+  const uint64_t t0 = (uint64_t)t * kRsTile;
+  const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
+  KT key[kRsIpt];
+  uint64_t val[kRsIpt];
+  uint32_t rank[kRsIpt];
+  unsigned dig[kRsIpt];
+  // warp w owns tile items [w*512, (w+1)*512): warp-major order is input order
 #pragma unroll
-    for (int k = 0; k < kRsIpt; ++k) {
-      uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
-      bool ok = idx < end;
-      key[k] = ok ? kin[idx] : KT(0);
-      val[k] = ok ? vin[idx] : 0ull;
-      dig[k] = ok ? (unsigned)((uint64_t)key[k] >> shift) & 0xffu : 0u;
-      unsigned valid = __ballot_sync(0xffffffffu, ok);
-      unsigned peers = digit_peers(dig[k], valid);
-      uint32_t c = ok ? wcnt[w][dig[k]] : 0u;
-      __syncwarp();
-      rank[k] = c + __popc(peers & lt);
-      if (ok && (peers & lt) == 0) wcnt[w][dig[k]] = c + __popc(peers);
-      __syncwarp();
-      if (!ok) dig[k] = 0xffffffffu;
+  for (int k = 0; k < kRsIpt; ++k) {
+    const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
+    const bool ok = idx < end;
+    key[k] = ok ? kin[idx] : KT(0);
+    val[k] = ok ? vin[idx] : 0ull;
+  }
+#pragma unroll
+  for (int k = 0; k < kRsIpt; ++k) {
+    const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
+    const bool ok = idx < end;
+    dig[k] = ok ? (unsigned)((uint64_t)key[k] >> shift) & 0xffu : 0u;
+    const unsigned peers = __match_any_sync(0xffffffffu, ok ? dig[k] : 0x100u);
+    const uint32_t c = ok ? wcnt[w][dig[k]] : 0u;
+    __syncwarp();
+    rank[k] = c + __popc(peers & lt);
+    if (ok && (peers & lt) == 0) wcnt[w][dig[k]] = c + __popc(peers);
+    __syncwarp();
+    if (!ok) dig[k] = 0xffffffffu;
+  }
+  __syncthreads();
+  // per digit: exclusive over warps, tile total, then the decoupled look-back
+  {
+    const int d = threadIdx.x;  // kRsThreads == kRsDigits
+    uint32_t sum = 0;
+#pragma unroll
+    for (int q = 0; q < kRsWarps; ++q) {
+      const uint32_t c = wcnt[q][d];
+      wcnt[q][d] = sum;
+      sum += c;
     }
-    __syncthreads();
-    // per digit: exclusive over warps, tile totals
-    for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x) {
-      uint32_t s = 0;
-#pragma unroll
-      for (int q = 0; q < kRsWarps; ++q) {
-        uint32_t c = wcnt[q][d];
-        wcnt[q][d] = s;
-        s += c;
+    ttot[d] = sum;
+    volatile unsigned long long* st = status + (uint64_t)t * kRsDigits + d;
+    if (t == 0) {
+      *st = kFlagPre | sum;
+      gpre[d] = 0;
+    } else {
+      *st = kFlagAgg | sum;
+      unsigned long long excl = 0;
+      int64_t k = (int64_t)t - 1;
+      for (;;) {
+        const unsigned long long v = *(volatile unsigned long long*)(status + (uint64_t)k * kRsDigits + d);
+        const unsigned long long flag = v & ~kValMask;
+        if (flag == 0) continue;  // predecessor not published yet
+        excl += v & kValMask;
+        if (flag == kFlagPre) break;
+        --k;
       }
-      ttot[d] = s;
+      *st = kFlagPre | (excl + sum);
+      gpre[d] = excl;
     }
-    __syncthreads();
-    {
-      uint32_t v = threadIdx.x < kRsDigits ? ttot[threadIdx.x] : 0u;
-      uint32_t tot;
-      uint32_t ex = block_excl_scan(v, shs, &tot);
-      if (threadIdx.x < kRsDigits) tstart[threadIdx.x] = ex;
-    }
-    __syncthreads();
+  }
+  __syncthreads();
+  {
+    uint32_t v = ttot[threadIdx.x];
+    uint32_t tot;
+    uint32_t ex = block_excl_scan(v, shs, &tot);
+    tstart[threadIdx.x] = ex;
+  }
+  __syncthreads();
 #pragma unroll
-    for (int k = 0; k < kRsIpt; ++k) {
-      if (dig[k] != 0xffffffffu) {
-        uint32_t pos = tstart[dig[k]] + wcnt[w][dig[k]] + rank[k];
-        skey[pos] = key[k];
-        sval[pos] = val[k];
-      }
+  for (int k = 0; k < kRsIpt; ++k) {
+    if (dig[k] != 0xffffffffu) {
+      const uint32_t pos = tstart[dig[k]] + wcnt[w][dig[k]] + rank[k];
+      skey[pos] = key[k];
+      sval[pos] = val[k];
     }
-    __syncthreads();
-    uint32_t tn = (uint32_t)((end - t0) < (uint64_t)kRsTile ? (end - t0) : (uint64_t)kRsTile);
-    for (uint32_t q = threadIdx.x; q < tn; q += blockDim.x) {
-      KT kk = skey[q];
-      unsigned d = (unsigned)((uint64_t)kk >> shift) & 0xffu;
-      uint32_t g = run_off[d] + (q - tstart[d]);
-      kout[g] = kk;
-      vout[g] = sval[q];
-    }
-    __syncthreads();
-    for (int d = threadIdx.x; d < kRsDigits; d += blockDim.x) run_off[d] += ttot[d];
-    __syncthreads();
+  }
+  __syncthreads();
+  const uint32_t tn = (uint32_t)(end - t0);
+  for (uint32_t q = threadIdx.x; q < tn; q += blockDim.x) {
+    const KT kk = skey[q];
+    const unsigned d = (unsigned)((uint64_t)kk >> shift) & 0xffu;
+    const uint64_t g = (uint64_t)gbase[d] + gpre[d] + (q - tstart[d]);
+    kout[g] = kk;
+    vout[g] = sval[q];
   }
 }
 
