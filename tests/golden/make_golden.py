@@ -184,9 +184,37 @@ def main():
         assert sum(ops) == a.n * b.n
         grids.append({"layout": enc_layout(a.layout), "a": enc_poly(a), "b": enc_poly(b), "l": l,
                       "bounds": [str(x) for x in bounds], "ops": ops})
+    # expression corpus (reference test_io.py:108-140 plus benchmark shapes):
+    # sha256 of the reference's format_poly(poly_from_expr(text)) with its own mul
+    from polymul.io import format_poly, poly_from_expr
+    fast = lambda a, b: mul(a, b, MulConfig(l=16, c=8))
+    exprs = []
+    corpus = [("0", "x y z"), ("7", "x y z"), ("x", "x y z"), ("x+y", "x y z"), ("x-x", "x y z"),
+              ("-x", "x y z"), ("2*x", "x y z"), ("x*y*z", "x y z"), ("x^3", "x y z"),
+              ("(x+y)^2", "x y z"), ("(1+x)*(1-x)", "x y z"), ("1+x*y^3", "x y z"),
+              ("(x+y)*(y+z)", "x y z"), ("((x))", "x y z"), ("x^2*x^3", "x y z"),
+              ("(1+x+y+z)^3-(1+x+y+z)^3", "x y z"), ("3-2", "x y z"), ("2^3", "x y z"),
+              ("1-x^2", "x y z"), ("(2*x+3*y)^2", "x y z"),
+              ("(1+x+y+z+t)^8", "x y z t"), ("(1+x+y+z+t)^8+1", "x y z t"),
+              ("(1+x+y+2*z^2+3*t^3+5*u^5)^5", "x y z t u"),
+              ("(1+u^2+v+w^2+x-y^2)^5", "u v w x y"), ("(1+u+v^2+w+x^2+y^3)^5+1", "u v w x y")]
+    for text, names in corpus:
+        for ct in (int, float):
+            lay = default_layout(tuple(names.split()))
+            p_ = poly_from_expr(text, lay, ct, mul=fast)
+            exprs.append({"text": text, "vars": names.split(), "ctype": ct.__name__, "n": p_.n,
+                          "sha256": hashlib.sha256(format_poly(p_).encode()).hexdigest()})
+    # the Fateman n=30 float operands exactly as the reference builds them
+    # (repeated squaring in float); their digest pins GPU float_ordered powering
+    lay4 = default_layout(("x", "y", "z", "t"))
+    for text in ("(1+x+y+z+t)^30", "(1+x+y+z+t)^30+1"):
+        p_ = poly_from_expr(text, lay4, float, mul=fast)
+        exprs.append({"text": text, "vars": ["x", "y", "z", "t"], "ctype": "float", "n": p_.n,
+                      "sha256": hashlib.sha256(format_poly(p_).encode()).hexdigest()})
     OUT.write_bytes(gzip.compress(json.dumps({"generator": "tests/golden/make_golden.py",
                                "reference": "polymul 0.1.0 (/root/reference/pkg)",
-                               "cases": cases, "grids": grids}, separators=(",", ":")).encode(), 9))
+                               "cases": cases, "grids": grids, "exprs": exprs},
+                               separators=(",", ":")).encode(), 9))
     print(f"wrote {len(cases)} product cases and {len(grids)} grid cases to {OUT}", file=sys.stderr)
 
 

@@ -256,3 +256,36 @@ def test_device_resident_api_and_free():
         want = mul(f, g, MulConfig(path="sort"))
         assert exps == want.exps and co == want.coeffs
         assert r.launches > 0 and "numeric" in r.phases
+
+
+def _gpu_ordered_mul(a, b):
+    return mul(a, b, MulConfig(float_ordered=True))
+
+
+def test_expression_corpus_with_gpu_mul():
+    from conftest import golden
+    from paper_1303_7425_b200.expr import poly_from_expr
+    for e in golden()["exprs"]:
+        if "^30" in e["text"]:
+            continue
+        lay = default_layout(tuple(e["vars"]))
+        ct = float if e["ctype"] == "float" else int
+        p = poly_from_expr(e["text"], lay, ct, mul=_gpu_ordered_mul)
+        assert p.n == e["n"] and io.poly_digest(p) == e["sha256"], e["text"]
+
+
+def test_fateman30_float_operands_and_product_bit_exact():
+    """The reference's float Fateman n=30 operands come from repeated squaring
+    in float (io.py:215-225); GPU powering in float_ordered mode reproduces
+    them bit for bit, and so the reference's float product digest too."""
+    from conftest import golden
+    from paper_1303_7425_b200.expr import poly_from_expr
+    want = {e["text"]: e for e in golden()["exprs"] if "^30" in e["text"]}
+    lay = default_layout(("x", "y", "z", "t"))
+    f = poly_from_expr("(1+x+y+z+t)^30", lay, float, mul=_gpu_ordered_mul)
+    g = poly_from_expr("(1+x+y+z+t)^30+1", lay, float, mul=_gpu_ordered_mul)
+    assert io.poly_digest(f) == want["(1+x+y+z+t)^30"]["sha256"]
+    assert io.poly_digest(g) == want["(1+x+y+z+t)^30+1"]["sha256"]
+    p = mul(f, g, MulConfig(float_ordered=True))
+    d = digests()["products"]["fateman30/float"]
+    assert p.n == d["n"] and io.poly_digest(p) == d["sha256"]
