@@ -60,6 +60,11 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-flush", action="store_true", help="diagnostic only: no L2 flush between steps")
+    ap.add_argument("--emulate-ranks", action="store_true",
+                    help="diagnostic: run the N>1 partition/gather path with gloo, every rank on "
+                         "cuda:0 (correctness only; timings are not meaningful)")
+    ap.add_argument("--verify", action="store_true",
+                    help="check the assembled product against the reference digest")
     return ap.parse_args()
 
 
@@ -186,6 +191,36 @@ def run_reference(args):
     return 0
 
 
+def verify_product(args, f, step, gathered, world, rank):
+    """sha256 of the reference text format of the (assembled) product vs the
+    reference's recorded digest (tests/golden/digests.json)."""
+    import numpy as np
+    from paper_1303_7425_b200 import io
+    from paper_1303_7425_b200.core import Polynomial
+    from paper_1303_7425_b200.parmul import limbs_to_ints
+    want = json.loads((ROOT / "tests" / "golden" / "digests.json").read_text())["products"]
+    key = f"{args.config}/{args.coeff}"
+    r = step()
+    if world > 1:
+        e, c = gathered[0]
+        exps = e.cpu().numpy().view(np.uint64)
+        words = c.cpu().numpy().view(np.uint64)
+    else:
+        e, c = r.tensors()
+        exps = e.cpu().numpy().view(np.uint64)
+        words = c.cpu().numpy().view(np.uint64).reshape(exps.shape[0], -1)
+    if r is not None:
+        r.free()
+    if args.coeff == "float":
+        co = words.reshape(-1).view(np.float64).tolist()
+    else:
+        co = limbs_to_ints(words, words.shape[1])
+    p = Polynomial._from_sorted(f.layout, exps.tolist(), co, float if args.coeff == "float" else int)
+    got = io.poly_digest(p)
+    ok = key in want and want[key]["sha256"] == got
+    return {"digest": got, "reference_digest": want.get(key, {}).get("sha256"), "ok": ok, "terms": p.n}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -201,11 +236,14 @@ def main():
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    local = 0 if args.emulate_ranks else int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.emulate_ranks:
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=dev)
     _native.load()
 
     f, g = operands(args)
@@ -238,8 +276,10 @@ def main():
             else:
                 e = torch.zeros(0, dtype=torch.int64, device=dev)
                 c = torch.zeros((0, 3), dtype=torch.int64, device=dev)
-            gather_slices(e, c)
+            gathered[0] = gather_slices(e, c)
         return res
+
+    gathered = [None]
 
     flush = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
@@ -366,6 +406,10 @@ def main():
             out["e2e"] = {"value": total_pairs * len(e2e_t) / sum(e2e_t), "unit": UNIT,
                           "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                           "ms_per_step": 1e3 * sum(e2e_t) / len(e2e_t)}
+    if args.verify:
+        out_v = verify_product(args, f, step, gathered, world, rank)
+        if out is not None:
+            out["verified"] = out_v
     if out is not None and world == 1 and not args.no_cpu_baseline:
         v, desc, pairs, dt = cpu_sample(f, g, 15.0, cpu_threads())
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port",

@@ -109,6 +109,8 @@ def gather_slices(exps, coef, group=None, device=None):
     import torch
     import torch.distributed as dist
     world = dist.get_world_size(group)
+    if dist.get_backend(group) != "nccl":  # gloo collectives run on host tensors
+        exps, coef = exps.cpu(), coef.cpu()
     n = torch.tensor([exps.shape[0]], dtype=torch.int64, device=exps.device)
     ns = [torch.zeros_like(n) for _ in range(world)]
     dist.all_gather(ns, n, group=group)
@@ -121,10 +123,18 @@ def gather_slices(exps, coef, group=None, device=None):
     pc = torch.zeros((m, w), dtype=torch.int64, device=exps.device)
     pe[:exps.shape[0]] = exps
     pc[:exps.shape[0]] = coef
-    ge = torch.empty(world * m, dtype=torch.int64, device=exps.device)
-    gc = torch.empty((world * m, w), dtype=torch.int64, device=exps.device)
-    dist.all_gather_into_tensor(ge, pe, group=group)
-    dist.all_gather_into_tensor(gc, pc, group=group)
+    if dist.get_backend(group) == "nccl":
+        ge = torch.empty(world * m, dtype=torch.int64, device=exps.device)
+        gc = torch.empty((world * m, w), dtype=torch.int64, device=exps.device)
+        dist.all_gather_into_tensor(ge, pe, group=group)
+        dist.all_gather_into_tensor(gc, pc, group=group)
+    else:  # gloo (CPU tests, single-GPU rank emulation): list all-gather on host tensors
+        pe, pc = pe.cpu(), pc.cpu()
+        le = [torch.empty_like(pe) for _ in range(world)]
+        lc = [torch.empty_like(pc) for _ in range(world)]
+        dist.all_gather(le, pe, group=group)
+        dist.all_gather(lc, pc, group=group)
+        ge, gc = torch.cat(le), torch.cat(lc)
     es = [ge[r * m:r * m + counts[r]] for r in range(world)]
     cs = [gc[r * m:r * m + counts[r]] for r in range(world)]
     return torch.cat(es), torch.cat(cs)
