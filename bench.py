@@ -63,6 +63,7 @@ def parse():
     ap.add_argument("--emulate-ranks", action="store_true",
                     help="diagnostic: run the N>1 partition/gather path with gloo, every rank on "
                          "cuda:0 (correctness only; timings are not meaningful)")
+    ap.add_argument("--clock-sampler", choices=["nvml", "nvidia-smi", "none"], default="nvml")
     ap.add_argument("--verify", action="store_true",
                     help="check the assembled product against the reference digest")
     return ap.parse_args()
@@ -75,6 +76,58 @@ def hbm_peak():
         return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
         return FALLBACK_HBM, "fallback (B200_PROFILING.md)"
+
+
+class NvmlClocks:
+    """In-process NVML sampling (SM clock, max clock, throttle reasons) during
+    the timed region, on a background thread; lighter than spawning nvidia-smi."""
+
+    REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
+               "sw_power_cap": 0x4}
+
+    def __init__(self, index: int, period_s: float = 0.25):
+        self.index = index
+        self.period = period_s
+        self.samples = []
+        self.stop_ev = None
+        self.th = None
+
+    def start(self):
+        import threading
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(self.index)
+            self.mx = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self.nv = None
+            return
+        self.stop_ev = threading.Event()
+
+        def run():
+            while not self.stop_ev.is_set():
+                try:
+                    sm = self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM)
+                    rs = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                    self.samples.append((sm, rs))
+                except Exception:
+                    pass
+                self.stop_ev.wait(self.period)
+
+        self.th = threading.Thread(target=run, daemon=True)
+        self.th.start()
+
+    def stop(self):
+        if self.nv is None or self.th is None:
+            return None
+        self.stop_ev.set()
+        self.th.join(timeout=2)
+        if not self.samples:
+            return None
+        reasons = sorted({k for _, rs in self.samples for k, bit in self.REASONS.items() if rs & bit})
+        return {"sm_mhz": statistics.median(s for s, _ in self.samples), "sm_max_mhz": self.mx,
+                "reasons": reasons, "samples": len(self.samples), "source": "nvml"}
 
 
 class Clocks:
@@ -288,11 +341,12 @@ def main():
             r.free()
     torch.cuda.synchronize()
 
-    clocks = Clocks(local)
+    clocks = {"nvml": NvmlClocks, "nvidia-smi": Clocks}.get(args.clock_sampler, lambda i: None)(local)
     if world > 1:
         dist.barrier()
     torch.cuda.synchronize()
-    clocks.start()
+    if clocks is not None:
+        clocks.start()
     times = []
     launches = 0
     last = None
@@ -314,7 +368,7 @@ def main():
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
-    ck = clocks.stop()
+    ck = clocks.stop() if clocks is not None else None
     my_ms = sum(times)
     t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
     if world > 1:

@@ -75,6 +75,8 @@ struct DeviceState {
   uint8_t* ws = nullptr;
   size_t ws_cap = 0;
   size_t ws_want = 0;  // high-water mark requested by previous calls
+  size_t mem_free0 = 0, mem_total = 0;  // device memory at first use (cudaMemGetInfo is
+                                        // slow and occasionally blocks for milliseconds)
   std::mutex mu;       // one product per device at a time uses the workspace
 };
 std::mutex g_mu;
@@ -90,6 +92,7 @@ int device_setup(int dev, cudaStream_t* st) {
     CUDA_TRY(cudaDeviceGetDefaultMemPool(&pool, dev));
     uint64_t thr = ~0ull;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
+    CUDA_TRY(cudaMemGetInfo(&d.mem_free0, &d.mem_total));
     d.init = true;
   }
   *st = d.stream;
@@ -160,6 +163,8 @@ int grow_workspace(DeviceState& d, cudaStream_t st) {
   d.ws_cap = 0;
   CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
   size_t want = std::min(d.ws_want + d.ws_want / 4, kWorkspaceMax);
+  if (getenv("PGPU_DEBUG"))
+    fprintf(stderr, "[pgpu] workspace grow %zu -> %zu bytes\n", d.ws_cap, want);
   if (want > freeb / 2) want = d.ws_want <= freeb / 2 ? d.ws_want : 0;  // keep room for the pool
   if (want == 0) return PGPU_OK;
   if (cudaMalloc((void**)&d.ws, want) != cudaSuccess) {
@@ -211,6 +216,7 @@ struct Timer {
 struct Ctx {
   cudaStream_t st;
   Arena* ar;
+  size_t mem_budget = 0;  // bytes this call may plan to use for large scratch
   Timer tm;
   int64_t launches = 0;
   int sms = 148;
@@ -241,6 +247,7 @@ struct Problem {
   void* ak;        // compact keys (uint32_t* or uint64_t*)
   void* bk;
   uint64_t KL, KH; // compact key range
+  uint64_t kmin, kmax;  // smallest / largest compact key of any pair
 };
 
 // A finished slice of the result (device buffers owned by the arena).
@@ -266,8 +273,10 @@ int range_rows(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint32_t**
   LAUNCHED(1);
   int g;
   LAUNCHED(device_scan<uint64_t>(pb.na, LenGen{*rlo, *rhi}, OffOut{*off}, part, &g, ctx.st));
-  CUDA_TRY(cudaMemcpyAsync(pairs, part + g, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  if (pairs) {
+    CUDA_TRY(cudaMemcpyAsync(pairs, part + g, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  }
   return PGPU_OK;
 }
 
@@ -524,8 +533,7 @@ int plan_batches(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t
 
 template <typename KT>
 int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice>& slices) {
-  size_t freeb = 0, totb = 0;
-  CUDA_TRY(cudaMemGetInfo(&freeb, &totb));
+  const size_t freeb = ctx.mem_budget;
   // per pair: records x2 (key + i<<32|j), segment starts; the segment outputs
   // (<= pairs, usually far fewer) and scan scratch fit in the remaining slack
   uint64_t bpp = 2 * (sizeof(KT) + 8) + 4 + 8;
@@ -677,11 +685,24 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
                                                    (const uint64_t*)pb.bk, pb.nb, S[s], dthr + s);
     LAUNCHED(1);
   }
-  unsigned long long thr[2];
+  // key ends (operands are ascending) travel back with the thresholds: one sync
+  unsigned long long* dends;
+  TRY(ctx.ar->alloc(&dends, 4));
+  if (pb.k32)
+    k_key_ends<uint32_t><<<1, 32, 0, ctx.st>>>((const uint32_t*)pb.ak, pb.na, (const uint32_t*)pb.bk,
+                                              pb.nb, dends);
+  else
+    k_key_ends<uint64_t><<<1, 32, 0, ctx.st>>>((const uint64_t*)pb.ak, pb.na, (const uint64_t*)pb.bk,
+                                              pb.nb, dends);
+  LAUNCHED(1);
+  unsigned long long thr[6];
   CUDA_TRY(cudaMemcpyAsync(thr, dthr, 16, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaMemcpyAsync(thr + 2, dends, 32, cudaMemcpyDeviceToHost, ctx.st));
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
   if (need[0]) pb.KL = thr[0];  // ~0 when no pair reaches lo: empty range
   if (need[1]) pb.KH = thr[1];  // ~0 when every pair is below hi
+  pb.kmin = thr[2] + thr[4];
+  pb.kmax = thr[3] + thr[5];
   return PGPU_OK;
 }
 
@@ -729,6 +750,7 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   TRY(grow_workspace(dstate, ctx.st));
   Arena ar(ctx.st, &dstate);
   ctx.ar = &ar;
+  ctx.mem_budget = dstate.mem_free0 > dstate.ws_cap ? dstate.mem_free0 - dstate.ws_cap : 0;
   ctx.tm.start(ctx.st, o.timing != 0);
 
   Problem pb;
@@ -746,8 +768,8 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   std::vector<Slice> slices;
   if (pb.KL < pb.KH) {
     // total pairs in range
-    uint64_t total = 0;
-    {
+    uint64_t total = (uint64_t)pb.na * pb.nb;
+    if (pb.KL > pb.kmin || pb.KH <= pb.kmax) {
       std::vector<uint64_t> bb{pb.KL}, cb;
       if (pb.k32) TRY(count_at<uint32_t>(ctx, pb, bb, cb)); else TRY(count_at<uint64_t>(ctx, pb, bb, cb));
       uint64_t below_lo = cb[0];

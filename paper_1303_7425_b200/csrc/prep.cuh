@@ -153,6 +153,18 @@ k_count_multi(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk,
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(cum + blockIdx.y, c);
 }
 
+// ends[0..3] = ak[0], ak[na-1], bk[0], bk[nb-1] (operands ascending)
+template <typename KT>
+__global__ void k_key_ends(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk,
+                           uint32_t nb, unsigned long long* ends) {
+  if (threadIdx.x == 0) {
+    ends[0] = ak[0];
+    ends[1] = ak[na - 1];
+    ends[2] = bk[0];
+    ends[3] = bk[nb - 1];
+  }
+}
+
 struct LenGen {
   const uint32_t* lo;
   const uint32_t* hi;
