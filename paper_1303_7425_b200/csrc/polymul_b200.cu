@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -175,6 +176,51 @@ int grow_workspace(DeviceState& d, cudaStream_t st) {
   d.ws_cap = want;
   return PGPU_OK;
 }
+
+// Pinned host buffers for host-side results: D2H into page-locked memory runs
+// at full PCIe/C2C speed, and reusing blocks avoids cudaMallocHost per call.
+// Blocks are tagged in pgpu_result._owner and come back via pgpu_free_result.
+struct PinnedPool {
+  std::mutex mu;
+  std::vector<std::pair<void*, size_t>> free_blocks;
+  static constexpr size_t kMaxCached = 8;
+  void* get(size_t bytes) {
+    {
+      std::lock_guard<std::mutex> lk(mu);
+      size_t best = SIZE_MAX;
+      int bi = -1;
+      for (size_t k = 0; k < free_blocks.size(); ++k)
+        if (free_blocks[k].second >= bytes && free_blocks[k].second < best) {
+          best = free_blocks[k].second;
+          bi = (int)k;
+        }
+      if (bi >= 0) {
+        void* p = free_blocks[bi].first;
+        free_blocks.erase(free_blocks.begin() + bi);
+        return p;
+      }
+    }
+    void* p = nullptr;
+    if (cudaMallocHost(&p, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    sizes_[p] = bytes;
+    return p;
+  }
+  void put(void* p) {
+    std::lock_guard<std::mutex> lk(mu);
+    if (free_blocks.size() >= kMaxCached) {
+      cudaFreeHost(free_blocks.front().first);
+      sizes_.erase(free_blocks.front().first);
+      free_blocks.erase(free_blocks.begin());
+    }
+    free_blocks.push_back({p, sizes_[p]});
+  }
+  std::map<void*, size_t> sizes_;
+};
+PinnedPool g_pinned;
+constexpr uintptr_t kPinnedTag = 0x50494e4e;  // result buffers come from g_pinned
 
 struct Timer {
   bool on = false;
@@ -823,9 +869,10 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
     out->exps = e;
     out->coeffs = c;
   } else {
-    out->exps = (uint64_t*)malloc(std::max<uint64_t>(n, 1) * 8);
-    out->coeffs = malloc(std::max<uint64_t>(n, 1) * 8 * nl);
-    if (!out->exps || !out->coeffs) return fail(PGPU_ENOMEM, "host allocation failed");
+    out->exps = (uint64_t*)g_pinned.get(std::max<uint64_t>(n, 1) * 8);
+    out->coeffs = g_pinned.get(std::max<uint64_t>(n, 1) * 8 * nl);
+    out->_owner = (void*)kPinnedTag;
+    if (!out->exps || !out->coeffs) return fail(PGPU_ENOMEM, "pinned host allocation failed");
     uint64_t at = 0;
     for (auto& s : slices) {
       CUDA_TRY(cudaMemcpyAsync(out->exps + at, s.exps, s.n * 8, cudaMemcpyDeviceToHost, ctx.st));
@@ -903,6 +950,9 @@ void pgpu_free_result(pgpu_result* r) {
     // the (retained) pool for the next product instead of to the driver
     if (r->exps) cudaFreeAsync(r->exps, 0);
     if (r->coeffs) cudaFreeAsync(r->coeffs, 0);
+  } else if (r->_owner == (void*)kPinnedTag) {
+    if (r->exps) g_pinned.put(r->exps);
+    if (r->coeffs) g_pinned.put(r->coeffs);
   } else {
     free(r->exps);
     free(r->coeffs);
