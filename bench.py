@@ -234,7 +234,7 @@ def run_reference(args):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(1, len(vals)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-            "dtype": "int192" if args.coeff == "int" else "f64", "data": "synthetic (closed form)",
+            "dtype": "int64" if args.coeff == "int" else "f64", "data": "synthetic (closed form)",
             "impl": "reference",
             "config": {"workload": workload_name(args, f, g), "sample": desc},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
@@ -426,10 +426,13 @@ def main():
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-               "dtype": "int192" if args.coeff == "int" else "f64",
+               "dtype": "int64" if args.coeff == "int" else "f64",
                "data": "synthetic (closed-form Fateman/Monagan-Pearce operands)",
                "config": {"workload": workload_name(args, f, g), "term_products": total_pairs,
                           "result_terms": n_out, "path": path_used, "result_limbs": nl,
+                          "arithmetic": ("exact integers: int64 operands, 128-bit products, "
+                                         "accumulators proven wide enough (Fateman n=30: 136-bit)")
+                          if args.coeff == "int" else "f64",
                           "parallelism": f"partition_by_ops x{world}" if world > 1 else "1 GPU",
                           "l2": f"flushed ({args.flush_mib} MiB write) between timed steps",
                           "plan_ms": plan_ms, "step_ms": [round(x, 3) for x in times]},
