@@ -52,7 +52,13 @@ k_gen(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __re
 // equal digits are contiguous.
 constexpr int kRsThreads = 256;
 constexpr int kRsWarps = kRsThreads / 32;
-constexpr int kRsIpt = 16;                         // items per thread per tile
+#ifndef PGPU_RS_MINB
+#define PGPU_RS_MINB 3
+#endif
+#ifndef PGPU_RS_IPT
+#define PGPU_RS_IPT 12
+#endif
+constexpr int kRsIpt = PGPU_RS_IPT;                // items per thread per tile
 constexpr int kRsTile = kRsThreads * kRsIpt;       // 4096
 constexpr int kRsDigits = 256;
 constexpr int kRsMaxPasses = 8;
@@ -116,7 +122,7 @@ __global__ void __launch_bounds__(kRsDigits) k_rs_hist_scan(unsigned int* ghist,
 }
 
 template <typename KT>
-__global__ void __launch_bounds__(kRsThreads)
+__global__ void __launch_bounds__(kRsThreads, PGPU_RS_MINB)
 k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* __restrict__ kout,
               uint64_t* __restrict__ vout, uint64_t n, int shift, const unsigned int* __restrict__ gbase,
               unsigned long long* status, unsigned int* tile_ctr) {
