@@ -25,6 +25,10 @@
  *   pgpu_last_error     exception messages (ValueError / ExponentOverflowError,
  *                       core.py:333-337, core.py:365-385)
  *   pgpu_device_count   (cluster node count; cluster.py:330)
+ *   pgpu_format         io.format_poly / io.write_poly term lines
+ *                       (io.py:241-248, io.py:306-308): the PolyFile text of a
+ *                       product, formatted on the device
+ *   pgpu_free_text      (ownership of the text; Python str in the reference)
  *
  * Every function returns a pgpu_status; on failure pgpu_last_error() holds a
  * message for the calling thread.  No function falls back to the CPU.
@@ -39,7 +43,7 @@ extern "C" {
 #endif
 
 #define PGPU_MAX_FIELDS 15
-#define PGPU_ABI_VERSION 1
+#define PGPU_ABI_VERSION 2
 
 typedef enum pgpu_status {
   PGPU_OK = 0,
@@ -138,6 +142,28 @@ int pgpu_count_below(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* 
                      uint64_t* cum);
 
 void pgpu_free_result(pgpu_result* r);
+
+/* PolyFile text of terms [begin, end) of p (reference io.format_poly,
+ * io.py:241-248, without its "vars ..." header line, whose names are not part
+ * of the packed layout): one "<coeff> <e_1> ... <e_m>\n" line per term, the
+ * exponents unpacked from `lay` (grlex degree field omitted), integers as
+ * Python str() (opt->coef_kind PGPU_I64 with opt->acc_limbs limbs of
+ * two's complement, or PGPU_I128), doubles as Python repr() (shortest
+ * round-trip digits).  Uses opt->device, stream, inputs_on_device (p's
+ * pointers are device pointers) and outputs_on_device (text stays on the
+ * device).  Release with pgpu_free_text. */
+typedef struct pgpu_text {
+  char* text;                       /* bytes, not NUL-terminated                */
+  int64_t bytes;
+  int32_t on_device;
+  int32_t _pad;
+  void* _owner;                     /* library bookkeeping                      */
+} pgpu_text;
+
+int pgpu_format(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64_t end,
+                const pgpu_options* opt, pgpu_text* out);
+void pgpu_free_text(pgpu_text* t);
+
 const char* pgpu_last_error(void);
 int pgpu_device_count(void);
 int pgpu_abi_version(void);

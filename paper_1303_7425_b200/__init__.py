@@ -9,8 +9,9 @@ library (lib/libpolymul_b200.so); there is no CPU fallback.
 
 from .core import (SENTINEL, CoefficientOverflowError, ExponentOverflowError, Layout, Polynomial,
                    VarTable, canonicalize, check_product_fits, default_layout)
-from .io import format_poly, poly_digest
-from .parmul import MulConfig, count_below, mul, native_mul
+from .arrays import ArrayPolynomial
+from .io import format_poly, format_text, poly_digest, text_digest, write_poly
+from .parmul import MulConfig, count_below, mul, mul_arrays, native_mul
 from .split import GridParams, SplitSet, select_grid
 from .cluster import ClusterPlan, gpu_mul, partition_by_ops
 
@@ -19,6 +20,7 @@ __version__ = "0.1.0"
 __all__ = [
     "SENTINEL", "CoefficientOverflowError", "ExponentOverflowError", "Layout", "Polynomial",
     "VarTable", "canonicalize", "check_product_fits", "default_layout", "format_poly",
-    "poly_digest", "MulConfig", "count_below", "mul", "native_mul", "GridParams", "SplitSet",
+    "poly_digest", "ArrayPolynomial", "format_text", "text_digest", "write_poly", "MulConfig",
+    "count_below", "mul", "mul_arrays", "native_mul", "GridParams", "SplitSet",
     "select_grid", "ClusterPlan", "gpu_mul", "partition_by_ops", "__version__",
 ]

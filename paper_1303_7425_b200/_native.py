@@ -22,7 +22,8 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpolymul_b200.so"
 
 # Every symbol include/polymul_b200.h declares (checked by the CPU test suite).
 EXPORTS = ("pgpu_default_options", "pgpu_mul", "pgpu_count_below", "pgpu_free_result",
-           "pgpu_last_error", "pgpu_device_count", "pgpu_abi_version")
+           "pgpu_format", "pgpu_free_text", "pgpu_last_error", "pgpu_device_count",
+           "pgpu_abi_version")
 
 
 class Layout(C.Structure):
@@ -48,6 +49,11 @@ class Result(C.Structure):
                 ("key_bits", C.c_int32), ("n_phase", C.c_int32),
                 ("phase_ms", C.c_float * NPHASE), ("phase_name", C.c_char_p * NPHASE),
                 ("_owner", C.c_void_p)]
+
+
+class Text(C.Structure):
+    _fields_ = [("text", C.c_void_p), ("bytes", C.c_int64), ("on_device", C.c_int32),
+                ("_pad", C.c_int32), ("_owner", C.c_void_p)]
 
 
 class NativeError(RuntimeError):
@@ -81,6 +87,11 @@ def load(path: Path | None = None) -> C.CDLL:
         lib.pgpu_count_below.restype = C.c_int
         lib.pgpu_free_result.argtypes = [C.POINTER(Result)]
         lib.pgpu_free_result.restype = None
+        lib.pgpu_format.argtypes = [C.POINTER(Poly), C.POINTER(Layout), C.c_int64, C.c_int64,
+                                    C.POINTER(Options), C.POINTER(Text)]
+        lib.pgpu_format.restype = C.c_int
+        lib.pgpu_free_text.argtypes = [C.POINTER(Text)]
+        lib.pgpu_free_text.restype = None
         lib.pgpu_last_error.argtypes = []
         lib.pgpu_last_error.restype = C.c_char_p
         lib.pgpu_device_count.argtypes = []

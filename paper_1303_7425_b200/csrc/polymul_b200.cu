@@ -28,6 +28,7 @@
 #include "../../include/polymul_b200.h"
 #include "common.cuh"
 #include "dense_path.cuh"
+#include "format.cuh"
 #include "prep.cuh"
 #include "scan.cuh"
 #include "sort_path.cuh"
@@ -889,6 +890,112 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   return PGPU_OK;
 }
 
+// PolyFile text of terms [begin, end) (reference io.format_poly, io.py:241-248).
+int format_impl(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64_t end,
+                const pgpu_options* opt, pgpu_text* out) {
+  if (!p || !lay || !out) return fail(PGPU_EINVAL, "null argument");
+  memset(out, 0, sizeof *out);
+  pgpu_options o;
+  if (opt) o = *opt; else pgpu_default_options(&o);
+  out->on_device = o.outputs_on_device;
+  if (lay->nfields < 1 || lay->nfields > PGPU_MAX_FIELDS)
+    return fail(PGPU_EINVAL, "layout needs 1..%d fields", PGPU_MAX_FIELDS);
+  if (begin < 0 || end > p->n || begin > end)
+    return fail(PGPU_EINVAL, "term range [%lld, %lld) outside [0, %lld)", (long long)begin,
+                (long long)end, (long long)p->n);
+  text::LineSpec spec;
+  memset(&spec, 0, sizeof spec);
+  int coef_digits;
+  size_t csz;
+  if (o.coef_kind == PGPU_F64) {
+    spec.kind = 0;
+    spec.nl = 1;
+    coef_digits = 24;  // "-d.dddddddddddddddde-308"
+    csz = 8;
+  } else if (o.coef_kind == PGPU_I64 || o.coef_kind == PGPU_I128) {
+    spec.kind = 1;
+    spec.nl = o.coef_kind == PGPU_I128 ? 2 : (o.acc_limbs ? o.acc_limbs : 1);
+    if (spec.nl < 1 || spec.nl > 3) return fail(PGPU_EINVAL, "integer width must be 1..3 limbs");
+    coef_digits = 1 + (spec.nl == 1 ? 20 : spec.nl == 2 ? 39 : 58);
+    csz = 8 * (size_t)spec.nl;
+  } else {
+    return fail(PGPU_EINVAL, "unknown coefficient kind");
+  }
+  const int first = lay->order == PGPU_GRLEX ? 1 : 0;  // the grlex degree is not printed
+  spec.nvars = lay->nfields - first;
+  uint32_t maxline = (uint32_t)coef_digits + 1;
+  for (int f = 0; f < spec.nvars; ++f) {
+    const int w = lay->width[first + f];
+    spec.shift[f] = lay->shift[first + f];
+    spec.mask[f] = w >= 64 ? ~0ull : ((1ull << w) - 1);
+    uint64_t m = spec.mask[f];
+    int d = 1;
+    while (m >= 10) {
+      m /= 10;
+      ++d;
+    }
+    maxline += 1 + (uint32_t)d;
+  }
+  const uint64_t n = (uint64_t)(end - begin);
+  if (n == 0) return PGPU_OK;
+
+  cudaStream_t lib_st;
+  TRY(device_setup(o.device, &lib_st));
+  Ctx ctx;
+  ctx.st = o.stream ? (cudaStream_t)o.stream : lib_st;
+  DeviceState& dstate = g_dev[o.device & 63];
+  std::lock_guard<std::mutex> ws_lock(dstate.mu);
+  TRY(grow_workspace(dstate, ctx.st));
+  Arena ar(ctx.st, &dstate);
+  ctx.ar = &ar;
+  const uint64_t* exps;
+  const void* coef;
+  if (o.inputs_on_device) {
+    exps = p->exps + begin;
+    coef = (const uint8_t*)p->coeffs + (size_t)begin * csz;
+  } else {
+    uint64_t* e;
+    uint8_t* c;
+    TRY(ar.alloc(&e, n));
+    TRY(ar.alloc(&c, n * csz));
+    CUDA_TRY(cudaMemcpyAsync(e, p->exps + begin, n * 8, cudaMemcpyHostToDevice, ctx.st));
+    CUDA_TRY(cudaMemcpyAsync(c, (const uint8_t*)p->coeffs + (size_t)begin * csz, n * csz,
+                             cudaMemcpyHostToDevice, ctx.st));
+    exps = e;
+    coef = c;
+  }
+  uint64_t* offs;
+  uint64_t* part;
+  TRY(ar.alloc(&offs, n + 1));
+  TRY(ar.alloc(&part, kMaxScanBlocks + 1));
+  int g = 0;
+  device_scan<uint64_t>(n, FmtLen{exps, coef, spec}, FmtOff{offs, n}, part, &g, ctx.st);
+  uint64_t total = 0;
+  CUDA_TRY(cudaMemcpyAsync(&total, offs + n, 8, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  char* dtext;
+  if (o.outputs_on_device) TRY(ar.alloc_out(&dtext, total));
+  else TRY(ar.alloc(&dtext, total));
+  const size_t smem = (size_t)kFmtThreads * maxline;
+  if (smem > 48 * 1024)
+    CUDA_TRY(cudaFuncSetAttribute(k_fmt_write, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const uint64_t blocks = (n + kFmtThreads - 1) / kFmtThreads;
+  k_fmt_write<<<(unsigned)blocks, kFmtThreads, smem, ctx.st>>>(exps, coef, spec, n, offs, dtext);
+  CUDA_TRY(cudaGetLastError());
+  if (o.outputs_on_device) {
+    ar.release(dtext);
+    out->text = dtext;
+  } else {
+    out->text = (char*)g_pinned.get(std::max<uint64_t>(total, 1));
+    if (!out->text) return fail(PGPU_ENOMEM, "pinned host allocation failed");
+    out->_owner = (void*)kPinnedTag;
+    CUDA_TRY(cudaMemcpyAsync(out->text, dtext, total, cudaMemcpyDeviceToHost, ctx.st));
+  }
+  out->bytes = (int64_t)total;
+  CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  return PGPU_OK;
+}
+
 }  // namespace
 
 extern "C" {
@@ -960,6 +1067,22 @@ void pgpu_free_result(pgpu_result* r) {
   r->exps = nullptr;
   r->coeffs = nullptr;
   r->n = 0;
+}
+
+int pgpu_format(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64_t end,
+                const pgpu_options* opt, pgpu_text* out) {
+  int r = format_impl(p, lay, begin, end, opt, out);
+  if (r != PGPU_OK && out) pgpu_free_text(out);
+  return r;
+}
+
+void pgpu_free_text(pgpu_text* t) {
+  if (!t || !t->text) return;
+  if (t->on_device) cudaFreeAsync(t->text, 0);
+  else if (t->_owner == (void*)kPinnedTag) g_pinned.put(t->text);
+  else free(t->text);
+  t->text = nullptr;
+  t->bytes = 0;
 }
 
 const char* pgpu_last_error(void) { return g_err.c_str(); }

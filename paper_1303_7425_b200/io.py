@@ -1,10 +1,25 @@
-"""PolyFile text writer (reference io.py:241-248), used as the golden-digest
-serializer: sha256(format_poly(product)) is the parity fingerprint recorded
-from the reference."""
+"""PolyFile text (reference io.py:241-248 `format_poly`, io.py:306-308
+`write_poly`): SURVEY 8(f) row 2, the on-disk format downstream of the
+product.
+
+`format_poly` / `poly_digest` here are the plain host serializers used as
+the golden-digest fingerprint (sha256 of the reference's format_poly,
+SURVEY.md Appendix A).  `format_text` / `write_poly` / `text_digest` are the
+product path: the term lines are formatted on the GPU by `pgpu_format`
+(csrc/format.cuh; integers as str(), doubles as repr()) in bounded chunks,
+straight from the product's arrays -- no Python int or float is created.
+"""
 
 from __future__ import annotations
 
+import ctypes as C
 import hashlib
+
+import numpy as np
+
+from . import _native as N
+
+DEFAULT_CHUNK_TERMS = 1 << 22
 
 
 def format_poly(poly) -> str:
@@ -19,3 +34,105 @@ def format_poly(poly) -> str:
 
 def poly_digest(poly) -> str:
     return hashlib.sha256(format_poly(poly).encode()).hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# GPU formatter
+# ---------------------------------------------------------------------------
+def header(layout) -> bytes:
+    return ("vars " + " ".join(layout.vars.names) + "\n").encode()
+
+
+def _arrays(p):
+    """(exps u64, coefficient array, coef_kind, limbs) of a Polynomial or
+    ArrayPolynomial, without building Python objects for ArrayPolynomial."""
+    from .arrays import ArrayPolynomial
+    ap = p if isinstance(p, ArrayPolynomial) else ArrayPolynomial.from_poly(p)
+    if ap.ctype is float:
+        return ap.exps_array(), ap.coef_array(), N.F64, 1
+    return ap.exps_array(), ap.coef_array(), N.I64, ap.nl
+
+
+def format_terms(exps: np.ndarray, coef: np.ndarray, kind: int, nl: int, layout,
+                 begin: int = 0, end: int | None = None, device: int = 0) -> bytes:
+    """Term lines [begin, end) of host arrays through pgpu_format."""
+    n = int(exps.shape[0])
+    end = n if end is None else end
+    if end <= begin:
+        return b""
+    lib = N.load()
+    exps = np.ascontiguousarray(exps, dtype=np.uint64)
+    coef = np.ascontiguousarray(coef)
+    poly = N.Poly(exps.ctypes.data, coef.ctypes.data, n)
+    o = N.default_options()
+    o.coef_kind = kind
+    o.acc_limbs = nl
+    o.device = device
+    lay = N.make_layout(layout)
+    t = N.Text()
+    st = lib.pgpu_format(C.byref(poly), C.byref(lay), begin, end, C.byref(o), C.byref(t))
+    if st != N.PGPU_OK:
+        from .parmul import _raise_status
+        _raise_status(st)
+    try:
+        return C.string_at(t.text, t.bytes) if t.bytes else b""
+    finally:
+        lib.pgpu_free_text(C.byref(t))
+
+
+def format_device(res, layout, begin: int = 0, end: int | None = None, device: int = 0) -> bytes:
+    """Term lines of a device-resident product (device.DeviceResult): the
+    formatter reads the result where the multiplier left it."""
+    end = res.n if end is None else end
+    if end <= begin:
+        return b""
+    lib = N.load()
+    poly = N.Poly(res.res.exps, res.res.coeffs, res.n)
+    o = N.default_options()
+    o.coef_kind = res.kind
+    o.acc_limbs = res.nl
+    o.device = device
+    o.inputs_on_device = 1
+    lay = N.make_layout(layout)
+    t = N.Text()
+    st = lib.pgpu_format(C.byref(poly), C.byref(lay), begin, end, C.byref(o), C.byref(t))
+    if st != N.PGPU_OK:
+        from .parmul import _raise_status
+        _raise_status(st)
+    try:
+        return C.string_at(t.text, t.bytes) if t.bytes else b""
+    finally:
+        lib.pgpu_free_text(C.byref(t))
+
+
+def iter_text(p, chunk_terms: int = DEFAULT_CHUNK_TERMS, device: int = 0):
+    """PolyFile bytes of p: the header, then the term lines in chunks of at
+    most chunk_terms terms (bounded host and device memory for any size)."""
+    exps, coef, kind, nl = _arrays(p)
+    yield header(p.layout)
+    n = int(exps.shape[0])
+    for b in range(0, n, chunk_terms):
+        yield format_terms(exps, coef, kind, nl, p.layout, b, min(n, b + chunk_terms), device)
+
+
+def format_text(p, device: int = 0) -> str:
+    """GPU-formatted equivalent of format_poly(p)."""
+    return b"".join(iter_text(p, device=device)).decode()
+
+
+def write_poly(path, p, device: int = 0, chunk_terms: int = DEFAULT_CHUNK_TERMS) -> int:
+    """reference io.write_poly (io.py:306-308) with GPU formatting; returns bytes written."""
+    total = 0
+    with open(path, "wb") as fh:
+        for part in iter_text(p, chunk_terms, device):
+            fh.write(part)
+            total += len(part)
+    return total
+
+
+def text_digest(p, device: int = 0, chunk_terms: int = DEFAULT_CHUNK_TERMS) -> str:
+    """sha256 of format_poly(p), formatted on the GPU chunk by chunk."""
+    h = hashlib.sha256()
+    for part in iter_text(p, chunk_terms, device):
+        h.update(part)
+    return h.hexdigest()

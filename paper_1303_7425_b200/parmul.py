@@ -80,6 +80,8 @@ class Operand:
 
     @classmethod
     def from_poly(cls, p, kind: int | None = None) -> "Operand":
+        if hasattr(p, "operand"):  # ArrayPolynomial: arrays straight through
+            return p.operand()
         exps = p.exps_array() if hasattr(p, "exps_array") else np.fromiter(p.exps, np.uint64, len(p.exps))
         if p.ctype is float:
             return cls(exps, np.asarray(p.coeffs, dtype=np.float64), N.F64)
@@ -244,7 +246,27 @@ def mul(a, b, cfg: MulConfig | None = None, *, split=None):
     return to_poly(cls, a.layout, a.ctype, raw)
 
 
+def mul_arrays(a, b, cfg: MulConfig | None = None, *, split=None):
+    """`mul` returning an ArrayPolynomial: the product stays in the arrays
+    the C ABI returns; Python lists are built only if
+    asked for.  Operands may be Polynomial or ArrayPolynomial."""
+    from .arrays import ArrayPolynomial
+    if cfg is None:
+        cfg = MulConfig()
+    check_compatible(a, b)
+    if a.is_zero or b.is_zero:
+        return ArrayPolynomial.zero(a.layout, a.ctype)
+    check_product_fits(a, b)
+    lo = 0 if split is None else int(split.bounds[0])
+    raw = native_mul(Operand.from_poly(a), Operand.from_poly(b), a.layout, lo=lo,
+                     path=cfg.path, float_ordered=cfg.float_ordered, device=cfg.device)
+    return ArrayPolynomial.from_raw(a.layout, a.ctype, raw)
+
+
 def to_poly(cls, layout, ctype, raw: RawProduct):
+    from .arrays import ArrayPolynomial
+    if isinstance(cls, type) and issubclass(cls, ArrayPolynomial):
+        return ArrayPolynomial.from_raw(layout, ctype, raw)
     exps = raw.exps.tolist()
     if ctype is float:
         coeffs = raw.coef.tolist()

@@ -52,7 +52,7 @@ def test_ctypes_struct_layouts_match_c(tmp_path):
 #include <stddef.h>
 #include "{HEADER}"
 int main(void) {{
-  printf("%zu %zu %zu %zu\\n", sizeof(pgpu_layout), sizeof(pgpu_poly), sizeof(pgpu_options), sizeof(pgpu_result));
+  printf("%zu %zu %zu %zu %zu\\n", sizeof(pgpu_layout), sizeof(pgpu_poly), sizeof(pgpu_options), sizeof(pgpu_result), sizeof(pgpu_text));
   printf("%zu %zu %zu\\n", offsetof(pgpu_options, lo), offsetof(pgpu_options, stream), offsetof(pgpu_result, phase_ms));
   return 0;
 }}''')
@@ -60,14 +60,15 @@ int main(void) {{
     subprocess.run(["gcc", "-o", str(exe), str(src)], check=True)
     lines = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout.split("\n")
     sizes = [int(x) for x in lines[0].split()]
-    assert sizes == [C.sizeof(N.Layout), C.sizeof(N.Poly), C.sizeof(N.Options), C.sizeof(N.Result)]
+    assert sizes == [C.sizeof(N.Layout), C.sizeof(N.Poly), C.sizeof(N.Options), C.sizeof(N.Result),
+                     C.sizeof(N.Text)]
     offs = [int(x) for x in lines[1].split()]
     assert offs == [N.Options.lo.offset, N.Options.stream.offset, N.Result.phase_ms.offset]
 
 
 def test_library_answers_without_a_gpu():
     lib = N.load()
-    assert lib.pgpu_abi_version() == 1
+    assert lib.pgpu_abi_version() == 2
     assert lib.pgpu_device_count() >= 0
     o = N.default_options()
     assert o.hi == (1 << 64) - 1 and o.lo == 0 and o.coef_kind == N.F64
