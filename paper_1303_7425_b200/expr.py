@@ -158,12 +158,17 @@ def variables_of(*texts) -> tuple:
     return tuple(seen)
 
 
+# the reference's benchmark examples (service/app.py:38-42)
+BENCH_EXAMPLES = {
+    1: ("(1+x+y+z+t)^{p}", "(1+x+y+z+t)^{p}+1"),
+    2: ("(1+x+y+2*z^2+3*t^3+5*u^5)^{p}", "(1+u+t+2*z^2+3*y^3+5*x^5)^{p}"),
+    3: ("(1+u^2+v+w^2+x-y^2)^{p}", "(1+u+v^2+w+x^2+y^3)^{p}+1"),
+}
+
+
 def bench_pair(example: int, p: int, ctype=int, mul=None):
-    """The reference's /bench operands (service/app.py:38-42, vars in order of
-    first appearance)."""
-    texts = {1: ("(1+x+y+z+t)^{p}", "(1+x+y+z+t)^{p}+1"),
-             2: ("(1+x+y+2*z^2+3*t^3+5*u^5)^{p}", "(1+u+t+2*z^2+3*y^3+5*x^5)^{p}"),
-             3: ("(1+u^2+v+w^2+x-y^2)^{p}", "(1+u+v^2+w+x^2+y^3)^{p}+1")}[example]
-    fa, fb = (t.format(p=p) for t in texts)
+    """The reference's /bench operands (service/app.py:38-42, 46-85: vars in
+    order of first appearance across both expressions)."""
+    fa, fb = (t.format(p=p) for t in BENCH_EXAMPLES[example])
     lay = default_layout(variables_of(fa, fb))
     return poly_from_expr(fa, lay, ctype, mul), poly_from_expr(fb, lay, ctype, mul)
