@@ -69,7 +69,10 @@ typedef enum pgpu_order { PGPU_GRLEX = 0, PGPU_LEX = 1 } pgpu_order;
 typedef enum pgpu_path {
   PGPU_PATH_AUTO = 0,
   PGPU_PATH_DENSE = 1,    /* sumset bytemap + per-interval private accumulators    */
-  PGPU_PATH_SORT = 2      /* expand / LSD radix sort / run-length reduce            */
+  PGPU_PATH_SORT = 2,     /* expand / LSD radix sort / run-length reduce            */
+  PGPU_PATH_BUCKET = 3    /* pairs written once into key-range buckets of <= 2048,
+                             each grouped and reduced by one CTA in shared memory
+                             (a batch that does not suit it takes PATH_SORT)       */
 } pgpu_path;
 
 /* Packed-exponent layout (reference Layout, core.py:65-121).  Fields are listed

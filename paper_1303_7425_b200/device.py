@@ -15,7 +15,7 @@ import numpy as np
 
 from . import _native as N
 from .core import SENTINEL
-from .parmul import PATHS, Operand, _raise_status
+from .parmul import PATH_NAMES, PATHS, Operand, _raise_status
 
 
 class DeviceOperand:
@@ -55,7 +55,7 @@ class DeviceResult:
         self.kind = int(res.coef_kind)
         self.pairs = int(res.pairs)
         self.launches = int(res.kernel_launches)
-        self.path = {1: "dense", 2: "sort"}.get(int(res.path_used), "none")
+        self.path = PATH_NAMES.get(int(res.path_used), "none")
         self.phases = {}
         for k in range(res.n_phase):
             nm = res.phase_name[k]

@@ -28,7 +28,8 @@ from .core import (SENTINEL, CoefficientOverflowError, ExponentOverflowError, ch
                    check_product_fits)
 
 MERGERS = ("heap", "tree")
-PATHS = {"auto": N.PATH_AUTO, "dense": N.PATH_DENSE, "sort": N.PATH_SORT}
+PATHS = {"auto": N.PATH_AUTO, "dense": N.PATH_DENSE, "sort": N.PATH_SORT, "bucket": N.PATH_BUCKET}
+PATH_NAMES = {1: "dense", 2: "sort", 3: "bucket"}
 DEFAULT_GRID_DENSITY = 64
 _M64 = (1 << 64) - 1
 
@@ -40,7 +41,7 @@ class MulConfig:
     l, c, merger  -- as in the reference; `merger` names the CPU merge the
                      reference would use and is validated the same way; both
                      produce identical output (merge.py:1-16), as does the GPU.
-    path          -- "auto" | "dense" | "sort" (device algorithm)
+    path          -- "auto" | "dense" | "sort" | "bucket" (device algorithm)
     float_ordered -- fold float coefficients in the reference's row order so
                      doubles are bit-identical to the CPU (sort path)
     device        -- CUDA ordinal
@@ -205,7 +206,7 @@ def native_mul(A: Operand, B: Operand, layout, *, lo: int = 0, hi: int = SENTINE
             name = res.phase_name[k]
             phases[name.decode() if name else f"phase{k}"] = float(res.phase_ms[k])
         return RawProduct(exps, coef, int(res.coef_kind), nl, int(res.pairs),
-                          {1: "dense", 2: "sort"}.get(int(res.path_used), "none"),
+                          PATH_NAMES.get(int(res.path_used), "none"),
                           int(res.kernel_launches), int(res.key_bits), phases)
     finally:
         lib.pgpu_free_result(C.byref(res))

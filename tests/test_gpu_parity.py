@@ -31,7 +31,7 @@ def _check(got, want, ordered_float=True, a=None, b=None):
         assert got.exps == [int(e) for e in want["exps"]]
 
 
-@pytest.mark.parametrize("path", ["auto", "sort"])
+@pytest.mark.parametrize("path", ["auto", "sort", "bucket"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_golden_cases(case, path):
     name, a, b, split, want = case
@@ -53,7 +53,7 @@ def test_golden_cases_dense_when_applicable(case):
 
 @pytest.mark.parametrize("cfg", ["fateman10/int", "fateman20/int", "fateman30/int", "mp12/int",
                                  "fateman10/float"])
-@pytest.mark.parametrize("path", ["auto", "sort"])
+@pytest.mark.parametrize("path", ["auto", "sort", "bucket"])
 def test_benchmark_digests(cfg, path):
     name, kind = cfg.split("/")
     f, g = benchpolys.CONFIGS[name](float if kind == "float" else int)
@@ -289,3 +289,25 @@ def test_fateman30_float_operands_and_product_bit_exact():
     p = mul(f, g, MulConfig(float_ordered=True))
     d = digests()["products"]["fateman30/float"]
     assert p.n == d["n"] and io.poly_digest(p) == d["sha256"]
+
+
+@pytest.mark.parametrize("name,want_path", [("mp12", ("bucket",)), ("fateman20", ("bucket", "sort"))])
+def test_bucket_path_choice_and_fallback(name, want_path):
+    """Sparse MP12 runs on the bucket path.  Fateman 20 forced onto it has
+    single keys with up to 3,951 pairs: such bins are reduced in the bucket
+    kernel's dense mode, or the batch falls back to the sort path (reported in
+    path_used); either way the result is the exact product."""
+    f, g = benchpolys.CONFIGS[name](int)
+    raw = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, path="bucket")
+    assert raw.path in want_path
+    ref = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, path="sort")
+    assert np.array_equal(raw.exps, ref.exps) and np.array_equal(raw.coef, ref.coef)
+
+
+def test_bucket_path_float_fast_mode_within_bound():
+    f, g = benchpolys.CONFIGS["mp12"](float)
+    fast = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, path="bucket")
+    exact = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, float_ordered=True)
+    assert fast.path == "bucket" and np.array_equal(fast.exps, exact.exps)
+    k = 114  # longest MP12 segment (SURVEY 8a)
+    assert np.all(np.abs(fast.coef - exact.coef) <= 2 * k * 2.0 ** -53 * np.abs(exact.coef))
