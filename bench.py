@@ -400,7 +400,12 @@ def main():
     out = None
     if rank == 0:
         peak, peak_src = hbm_peak()
-        kern = "numeric" if "numeric" in phases else ("sort" if "sort" in phases else None)
+        if "numeric" in phases:
+            kern = "numeric"
+        elif path_used == "bucket" and "reduce" in phases:
+            kern = "reduce"
+        else:
+            kern = "sort" if "sort" in phases else None
         kern_ms = phases.get(kern, float("nan")) if kern else float("nan")
         w_c = 8 if args.coeff == "float" else 8 * nl
         w_in = 8 if A.kind != 2 else 16
@@ -414,7 +419,9 @@ def main():
                 traffic = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
-        roof = {"bound": "hbm", "kernel": f"k_numeric ({path_used} path)" if kern == "numeric" else kern,
+        kname = {"numeric": f"k_numeric ({path_used} path)", "reduce": "k_bucket_reduce (bucket path)",
+                 "sort": "k_rs_onesweep passes (sort path)"}.get(kern, kern)
+        roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
                 "peak_source": peak_src, "kernel_ms": kern_ms,
