@@ -48,9 +48,16 @@ namespace pgpu {
 // keys of dense operands) and then writes only the marked bytes to the global
 // bytemap.  Wider tiles store straight to global memory.  Stores are
 // idempotent byte writes of 1: no atomics, independent of order.
+#ifndef PGPU_SYM_UNROLL
+#define PGPU_SYM_UNROLL 4
+#endif
+constexpr int kSymUnroll = PGPU_SYM_UNROLL;
 constexpr int kSymRows = 64;
 constexpr int kSymCols = 256;
-constexpr uint32_t kSymWin = 65536;
+#ifndef PGPU_SYM_WIN
+#define PGPU_SYM_WIN 65536
+#endif
+constexpr uint32_t kSymWin = PGPU_SYM_WIN;
 
 template <typename KT>
 __global__ void __launch_bounds__(256)
@@ -91,9 +98,10 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
       const uint64_t ai = sa[i - r0];
       if (local) {
         const uint32_t ao = (uint32_t)(ai + (uint64_t)bk[c0] - wlo);  // offset of column c0
-        const uint64_t b0 = (uint64_t)sb[0];
-        for (uint32_t j = lo + lane; j < hi; j += 32)
-          win[ao + (uint32_t)((uint64_t)sb[j - c0] - b0)] = 1;
+        const uint32_t b0 = (uint32_t)sb[0];
+        const uint32_t aob = ao - b0;  // window offset = aob + bk (mod 2^32; the sum is in range)
+#pragma unroll kSymUnroll
+        for (uint32_t j = lo + lane; j < hi; j += 32) win[aob + (uint32_t)sb[j - c0]] = 1;
       } else {
         const uint64_t a = ai - R0;
         for (uint32_t j = lo + lane; j < hi; j += 32) bytemap[a + (uint64_t)sb[j - c0]] = 1;
