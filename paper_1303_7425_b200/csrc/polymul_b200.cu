@@ -115,8 +115,11 @@ struct Arena {
   size_t used = 0;
   size_t requested = 0;
   std::vector<void*> ptrs;  // cudaMallocAsync allocations owned by the arena
+  uint8_t* blk = nullptr;   // caller-provided block (batch scratch): any item size
+  size_t blk_cap = 0;
   explicit Arena(cudaStream_t s, DeviceState* d = nullptr, size_t base = 0)
       : st(s), dev(d), used(base), requested(base) {}
+  Arena(cudaStream_t s, uint8_t* block, size_t cap) : st(s), blk(block), blk_cap(cap) {}
   ~Arena() {
     for (void* p : ptrs) cudaFreeAsync(p, st);
     if (dev && requested > dev->ws_want) dev->ws_want = requested;
@@ -125,6 +128,14 @@ struct Arena {
   int alloc(T** p, size_t count) {
     size_t bytes = std::max<size_t>(count * sizeof(T), 16);
     bytes = (bytes + 255) & ~size_t(255);
+    if (blk) {
+      if (used + bytes <= blk_cap) {
+        *p = reinterpret_cast<T*>(blk + used);
+        used += bytes;
+        return PGPU_OK;
+      }
+      return alloc_fresh(p, bytes);
+    }
     if (bytes > kWorkspaceMaxItem) return alloc_fresh(p, bytes);  // big batch buffers: pool only
     requested += bytes;
     if (dev && dev->ws && used + bytes <= dev->ws_cap) {
@@ -264,6 +275,8 @@ struct Timer {
 struct Ctx {
   cudaStream_t st;
   Arena* ar;
+  uint8_t* batch_blk = nullptr;  // one block reused by every batch of a product
+  size_t batch_cap = 0;
   size_t mem_budget = 0;  // bytes this call may plan to use for large scratch
   Timer tm;
   int64_t launches = 0;
@@ -396,49 +409,64 @@ int radix_sort(Ctx& ctx, KT** keys, uint64_t** vals, KT* kalt, uint64_t* valt, u
   return PGPU_OK;
 }
 
+template <typename KT, typename RT>
+int sort_range_rt(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
+                  uint64_t pairs, int bits, Slice* out);
+
+// local key width: keys are stored relative to KL, in 32 bits when they fit
 template <typename KT>
 int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
-                    uint64_t pairs, Slice* out);
+                    uint64_t pairs, Slice* out) {
+  out->n = 0;
+  if (pairs == 0) return PGPU_OK;
+  uint64_t kmax_local = (KH == ~0ull ? ((pb.P.kbits >= 64) ? ~0ull : ((1ull << pb.P.kbits) - 1))
+                                     : KH - 1) - KL;
+  int bits = bitlen64(kmax_local);
+  if (bits <= 32) return sort_range_rt<KT, uint32_t>(ctx, outer, pb, KL, KH, pairs, bits, out);
+  return sort_range_rt<KT, uint64_t>(ctx, outer, pb, KL, KH, pairs, bits, out);
+}
 
 // One batch: its scratch lives in a batch-scoped arena (returned to the pool
 // before the next batch); only the compacted output is owned by the caller's arena.
 template <typename KT>
 int sort_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t pairs, Slice* out) {
   Arena* outer = ctx.ar;
+  int r;
+  if (ctx.batch_blk) {  // large products: the batch block allocated once per product
+    Arena batch(ctx.st, ctx.batch_blk, ctx.batch_cap);
+    ctx.ar = &batch;
+    r = sort_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out);
+    ctx.ar = outer;
+    return r;
+  }
   // nested: small batches bump-allocate above the caller's workspace usage
   Arena batch(ctx.st, pairs * 48 < (64ull << 20) ? outer->dev : nullptr, outer->used);
   ctx.ar = &batch;
-  int r = sort_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out);
+  r = sort_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out);
   ctx.ar = outer;
   return r;
 }
 
-template <typename KT>
-int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
-                    uint64_t pairs, Slice* out) {
-  out->n = 0;
-  if (pairs == 0) return PGPU_OK;
+template <typename KT, typename RT>
+int sort_range_rt(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
+                  uint64_t pairs, int bits, Slice* out) {
   uint32_t *rlo, *rhi;
   uint64_t* off;
   uint64_t chk;
   TRY(range_rows<KT>(ctx, pb, KL, KH, &rlo, &rhi, &off, &chk));
   if (chk != pairs) return fail(PGPU_ECUDA, "pair count mismatch %llu vs %llu",
                                 (unsigned long long)chk, (unsigned long long)pairs);
-  // local key width: keys are stored relative to KL
-  uint64_t kmax_local = (KH == ~0ull ? ((pb.P.kbits >= 64) ? ~0ull : ((1ull << pb.P.kbits) - 1))
-                                     : KH - 1) - KL;
-  int bits = bitlen64(kmax_local);
-  KT *keys, *kalt;
+  RT *keys, *kalt;
   uint64_t *vals, *valt;
   TRY(ctx.ar->alloc(&keys, pairs));
   TRY(ctx.ar->alloc(&vals, pairs));
   TRY(ctx.ar->alloc(&kalt, pairs));
   TRY(ctx.ar->alloc(&valt, pairs));
-  k_gen<KT><<<grid_for((int64_t)pb.na * 32, 256, ctx.sms * 16), 256, 0, ctx.st>>>(
+  k_gen<KT, RT><<<grid_for((int64_t)pb.na * 32, 256, ctx.sms * 16), 256, 0, ctx.st>>>(
       (const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, off, pb.na, KL, keys, vals);
   LAUNCHED(1);
   ctx.tm.mark(1, "gen");
-  TRY(radix_sort<KT>(ctx, &keys, &vals, kalt, valt, pairs, bits));
+  TRY(radix_sort<RT>(ctx, &keys, &vals, kalt, valt, pairs, bits));
   ctx.tm.mark(2, "sort");
   // heads -> segment starts (reuse the spare buffer as starts)
   uint32_t* starts;
@@ -446,7 +474,7 @@ int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint
   uint32_t* part;
   TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
   int g;
-  LAUNCHED(device_scan<uint32_t>(pairs, HeadGen<KT>{keys}, HeadOut{starts}, part, &g, ctx.st));
+  LAUNCHED(device_scan<uint32_t>(pairs, HeadGen<RT>{keys}, HeadOut{starts}, part, &g, ctx.st));
   uint32_t nseg;
   CUDA_TRY(cudaMemcpyAsync(&nseg, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
@@ -460,12 +488,12 @@ int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint
   TRY(ctx.ar->alloc(&snz, nseg));
   int gr = grid_for(nseg, 256, 1 << 30);
   if (pb.ck == PGPU_F64) {
-    k_seg_reduce_f64<KT><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, (const double*)pb.acoef,
+    k_seg_reduce_f64<RT><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, (const double*)pb.acoef,
                                                 (const double*)pb.bcoef, KL, pb.P, sexp,
                                                 (double*)scoef, snz);
   } else {
 #define SEGRED(NL_, CK_)                                                                   \
-  k_seg_reduce_int<KT, NL_, CK_><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, pb.acoef, \
+  k_seg_reduce_int<RT, NL_, CK_><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, pb.acoef, \
                                                          pb.bcoef, KL, pb.P, sexp, scoef, snz)
     if (pb.ck == PGPU_I64) {
       if (nl == 1) SEGRED(1, 1); else if (nl == 2) SEGRED(2, 1); else SEGRED(3, 1);
@@ -493,13 +521,18 @@ int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint
 }
 
 // Split [KL, KH) into ranges of at most `cap` pairs, in ascending key order.
+// max_span (0 = none): also keep every range's key span within max_span, so
+// that its records carry 32-bit local keys (4 radix passes of 12-byte records
+// instead of 5 of 16 bytes for 33..40-bit compact keys).
 template <typename KT>
 int plan_batches(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t total,
                  uint64_t cap, std::vector<std::pair<uint64_t, uint64_t>>& ranges,
-                 std::vector<uint64_t>& counts) {
+                 std::vector<uint64_t>& counts, uint64_t max_span = 0) {
   ranges.clear();
   counts.clear();
-  if (total <= cap) {
+  const uint64_t keyend = pb.kmax + 1;  // effective end of the open top range
+  auto eff = [&](uint64_t b) { return b == ~0ull ? keyend : b; };
+  if (total <= cap && (max_span == 0 || eff(KH) - KL <= max_span)) {
     ranges.push_back({KL, KH});
     counts.push_back(total);
     return PGPU_OK;
@@ -553,7 +586,7 @@ int plan_batches(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t
       // bound the open top by the largest possible key + 1
       hiK = ak[pb.na - 1] + bk[pb.nb - 1] + 1;
     }
-    if (c > cap && hiK - bnd[k] > 1) {
+    if ((c > cap || (max_span && hiK - bnd[k] > max_span)) && hiK - bnd[k] > 1) {
       uint64_t mid = bnd[k] + (hiK - bnd[k]) / 2;
       std::vector<uint64_t> cc, bb{mid};
       TRY(count_at<KT>(ctx, pb, bb, cc));
@@ -571,7 +604,9 @@ int plan_batches(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t
   size_t k = 0;
   while (k + 1 < bnd.size()) {
     size_t e = k + 1;
-    while (e + 1 < bnd.size() && cm[e + 1] - cm[k] <= cap) ++e;
+    while (e + 1 < bnd.size() && cm[e + 1] - cm[k] <= cap &&
+           (max_span == 0 || eff(bnd[e + 1]) - bnd[k] <= max_span))
+      ++e;
     ranges.push_back({bnd[k], bnd[e]});
     counts.push_back(cm[e] - cm[k]);
     k = e;
@@ -796,7 +831,35 @@ int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice
   if (env) cap = std::min<uint64_t>(cap, strtoull(env, nullptr, 10));
   std::vector<std::pair<uint64_t, uint64_t>> ranges;
   std::vector<uint64_t> counts;
-  TRY(plan_batches<KT>(ctx, pb, pb.KL, pb.KH, total, cap, ranges, counts));
+  // wide operand keys: batches narrow enough for 32-bit record keys, unless
+  // that would take more than a few dozen extra batches
+  uint64_t max_span = 0;
+  if (!pb.k32) {
+    const uint64_t span = (pb.KH == ~0ull ? pb.kmax + 1 : pb.KH) - pb.KL;
+    if ((span >> 32) <= 48 && !getenv("PGPU_NO_SPAN32")) max_span = 0xffffffffull;
+  }
+  TRY(plan_batches<KT>(ctx, pb, pb.KL, pb.KH, total, cap, ranges, counts, max_span));
+  // Products with several large batches: one scratch block sized for the
+  // largest batch serves them all (per-batch pool allocations of tens of GB
+  // made run times vary by up to 2x through physical remapping).
+  uint64_t maxc = 0;
+  for (uint64_t c : counts) maxc = std::max(maxc, c);
+  const size_t blk_bytes = (size_t)maxc * bpp + (256ull << 20);
+  if (ranges.size() > 1 && blk_bytes > (1ull << 30)) {
+    if (cudaMallocAsync((void**)&ctx.batch_blk, blk_bytes, ctx.st) == cudaSuccess) {
+      ctx.batch_cap = blk_bytes;
+    } else {
+      cudaGetLastError();
+      ctx.batch_blk = nullptr;
+    }
+  }
+  struct BlkFree {
+    Ctx& c;
+    ~BlkFree() {
+      if (c.batch_blk) cudaFreeAsync(c.batch_blk, c.st);
+      c.batch_blk = nullptr;
+    }
+  } blk_free{ctx};
   for (size_t r = 0; r < ranges.size(); ++r) {
     Slice s;
     bool done = false;

@@ -23,11 +23,13 @@ namespace pgpu {
 // One warp per row, lanes over consecutive columns: coalesced key loads and
 // coalesced record stores.  Row i's pairs land at off[i] in increasing j, rows
 // in increasing i, so the generation order is the reference's (i, j) order.
-template <typename KT>
+// KT: operand compact keys; RT: record keys (key - KL), u32 when the batch's
+// key span fits 32 bits even if the operands' keys do not.
+template <typename KT, typename RT>
 __global__ void __launch_bounds__(256)
 k_gen(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
       const uint32_t* __restrict__ rhi, const uint64_t* __restrict__ off, uint32_t na,
-      uint64_t KL, KT* __restrict__ keys, uint64_t* __restrict__ vals) {
+      uint64_t KL, RT* __restrict__ keys, uint64_t* __restrict__ vals) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nwarps) {
@@ -36,7 +38,7 @@ k_gen(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __re
     uint64_t base = off[i] - j0;
     uint64_t ai = (uint64_t)ak[i] - KL;  // wraps for rows below KL; the sum does not
     for (uint32_t j = j0 + lane; j < j1; j += 32) {
-      keys[base + j] = (KT)(ai + (uint64_t)__ldg(bk + j));
+      keys[base + j] = (RT)(ai + (uint64_t)__ldg(bk + j));
       vals[base + j] = ((uint64_t)i << 32) | j;
     }
   }
