@@ -67,5 +67,26 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
     return target
 
 
+def build_pylimbs(force: bool = False) -> Path:
+    """The CPython marshaling helper (csrc/pylimbs.c), built with gcc in-tree."""
+    import sysconfig
+    src = CSRC / "pylimbs.c"
+    out = LIBDIR / ("_pylimbs" + sysconfig.get_config_var("EXT_SUFFIX"))
+    if out.exists() and not force and out.stat().st_mtime >= src.stat().st_mtime:
+        return out
+    LIBDIR.mkdir(exist_ok=True)
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        raise RuntimeError("gcc not found: cannot build the marshaling helper")
+    tmp = out.with_suffix(".tmp")
+    cmd = [cc, "-O2", "-shared", "-fPIC", "-I", sysconfig.get_paths()["include"], str(src), "-o", str(tmp)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    if res.returncode != 0:
+        raise RuntimeError(f"gcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")
+    os.replace(tmp, out)
+    return out
+
+
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_pylimbs(force="--force" in sys.argv))

@@ -111,15 +111,41 @@ def int_coeff_array(coeffs, kind: int | None = None):
     return out, N.I128
 
 
+_PYLIMBS = None
+
+
+def _pylimbs():
+    """The C marshaling helper (csrc/pylimbs.c, lib/_pylimbs*.so), or None."""
+    global _PYLIMBS
+    if _PYLIMBS is None:
+        _PYLIMBS = False
+        try:
+            import importlib.util
+            import sysconfig
+            from pathlib import Path
+            path = Path(__file__).resolve().parent / "lib" / ("_pylimbs" + sysconfig.get_config_var("EXT_SUFFIX"))
+            if path.exists():
+                spec = importlib.util.spec_from_file_location("_pylimbs", path)
+                mod = importlib.util.module_from_spec(spec)
+                spec.loader.exec_module(mod)
+                _PYLIMBS = mod
+        except Exception:  # marshaling only: the Python conversion below is equivalent
+            _PYLIMBS = False
+    return _PYLIMBS or None
+
+
 def limbs_to_ints(limbs: np.ndarray, nl: int) -> list:
     """(n, nl) u64 two's-complement limbs -> Python ints.
 
-    Values that fit int64 go through numpy's tolist; the rest are built with
-    int.from_bytes on their little-endian limb bytes (about 2x faster than
-    shifting limbs together in Python)."""
+    Built in C by the marshaling helper when it is present (about 5x faster);
+    otherwise values that fit int64 go through numpy's tolist and the rest
+    through int.from_bytes on their little-endian limb bytes."""
     if limbs.size == 0:
         return []
     limbs = np.ascontiguousarray(limbs.reshape(-1, nl))
+    helper = _pylimbs()
+    if helper is not None:
+        return helper.limbs_to_list(memoryview(limbs).cast("B"), limbs.shape[0], nl)
     lo = limbs[:, 0].view(np.int64)
     if nl == 1:
         return lo.tolist()

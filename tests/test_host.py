@@ -147,3 +147,22 @@ def test_oracle_count_ops_sums_to_all_pairs(rng):
     bounds = select_grid(a, b, GridParams(5)).bounds
     ops = [O.count_ops(a, b, bounds[k], bounds[k + 1]) for k in range(len(bounds) - 1)]
     assert sum(ops) == a.n * b.n
+
+
+def test_limb_marshaling_helper_matches_python_ints():
+    """csrc/pylimbs.c (C marshaling of result limbs) == the pure-Python conversion."""
+    import random
+    from paper_1303_7425_b200 import parmul
+    from paper_1303_7425_b200.arrays import int_limbs
+    from paper_1303_7425_b200.build import build_pylimbs
+    build_pylimbs()
+    parmul._PYLIMBS = None
+    assert parmul._pylimbs() is not None
+    R = random.Random(3)
+    for nl in (1, 2, 3):
+        B = 64 * nl
+        vals = [R.randrange(-2 ** (B - 1), 2 ** (B - 1)) >> R.randrange(0, B) for _ in range(20000)]
+        vals += [0, -1, 2 ** (B - 1) - 1, -2 ** (B - 1), 2 ** 63 - 1, -2 ** 63]
+        vals = [v for v in vals if -2 ** (B - 1) <= v < 2 ** (B - 1)]
+        arr, _ = int_limbs(vals, nl)
+        assert parmul.limbs_to_ints(arr, nl) == vals
