@@ -386,9 +386,18 @@ k_numeric(NumArgs A) {
       for (int u = 0; u < kUnroll; ++u) {
         const uint32_t j = c + lane + 32 * u;
         const KT key = (KT)(akr + bkr[32 * u]);  // bk is padded: the load is in bounds
-        const uint64_t dk = (uint64_t)key - Klo;  // wraps for keys below Klo
-        const bool ok = j < nb && (uint64_t)key >= Klo && dk <= span_t;
-        const uint32_t off = (uint32_t)dk;
+        bool ok;
+        uint32_t off;
+        if constexpr (sizeof(KT) == 4) {
+          // 32-bit keys: the interval bounds fit 32 bits too; an offset that
+          // wraps (key below Klo) exceeds the span, so one compare suffices
+          off = (uint32_t)key - (uint32_t)Klo;
+          ok = j < nb && off <= (uint32_t)span_t;
+        } else {
+          const uint64_t dk = (uint64_t)key - Klo;  // wraps for keys below Klo
+          ok = j < nb && dk <= span_t;
+          off = (uint32_t)dk;
+        }
         nv += __popc(__ballot_sync(0xffffffffu, ok));
         uint32_t sl;
         if constexpr (TBL) {
