@@ -736,7 +736,10 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   }
   ctx.tm.mark(1, "gen");
   const int nl = pb.nl ? pb.nl : 1;
-  const uint64_t scap = std::min<uint64_t>(pairs, std::max<uint64_t>(pairs / 4, 1ull << 16));
+  // staging holds every distinct term in the worst case (sparse products with
+  // few collisions have almost as many terms as pairs); batches here are
+  // <= 2^28 pairs, so this is at most 2^28 * 32 B
+  const uint64_t scap = pairs;
   uint64_t *sexp, *scoef, *bbase;
   uint32_t* bnnz;
   unsigned long long* sctr;

@@ -181,11 +181,12 @@ def test_batched_sort_path_matches_single_batch(monkeypatch):
     assert batched.exps == whole.exps and batched.coeffs == whole.coeffs
 
 
-@pytest.mark.parametrize("path", ["dense", "sort"])
-def test_disjoint_ranges_concatenate_to_the_product(path):
+@pytest.mark.parametrize("path,name", [("dense", "fateman8"), ("sort", "fateman8"),
+                                       ("bucket", "fateman8"), ("bucket", "mp6"), ("sort", "mp6")])
+def test_disjoint_ranges_concatenate_to_the_product(path, name):
     """The multi-GPU contract: products restricted to consecutive packed ranges
     [S_k, S_k+1) concatenate to the full product (split.py:5-9)."""
-    f, g = benchpolys.fateman(8)
+    f, g = benchpolys.fateman(8) if name == "fateman8" else benchpolys.monagan_pearce(6)
     A, B = Operand.from_poly(f), Operand.from_poly(g)
     full = native_mul(A, B, f.layout, path=path)
     bounds = select_grid(f, g, GridParams(5)).bounds
@@ -223,7 +224,7 @@ def test_dense_float_matches_oracle_within_bound(rng):
             assert abs(gd.get(e, 0.0) - wd.get(e, 0.0)) <= tol
 
 
-@pytest.mark.parametrize("path", ["dense", "sort"])
+@pytest.mark.parametrize("path", ["dense", "sort", "bucket"])
 def test_int128_operands_signed(path, rng):
     """Operands beyond 63 bits (two-limb int128) with mixed signs."""
     from paper_1303_7425_b200.core import Polynomial as P
@@ -311,3 +312,26 @@ def test_bucket_path_float_fast_mode_within_bound():
     assert fast.path == "bucket" and np.array_equal(fast.exps, exact.exps)
     k = 114  # longest MP12 segment
     assert np.all(np.abs(fast.coef - exact.coef) <= 2 * k * 2.0 ** -53 * np.abs(exact.coef))
+
+
+@pytest.mark.parametrize("ctype", [int, float])
+def test_bucket_path_random_sparse_vs_oracle(ctype, rng):
+    """Random sparse operands (few repeated keys, signed coefficients) through
+    the bucket path against the oracle: exact for ints, within the reordering
+    bound for floats."""
+    from oracle import oracle as O
+    from paper_1303_7425_b200.core import Polynomial as P
+    lay = default_layout(("x", "y", "z", "t"))
+    for _ in range(3):
+        terms = lambda n: [((rng.randint(-10 ** 6, 10 ** 6) if ctype is int else rng.uniform(-3, 3)),
+                            tuple(rng.randint(0, 40) for _ in range(4))) for _ in range(n)]
+        a, b = P(lay, terms(2000), ctype), P(lay, terms(1500), ctype)
+        got = native_mul(Operand.from_poly(a), Operand.from_poly(b), lay, path="bucket")
+        want = O.mul(a, b)
+        assert got.path == "bucket"
+        assert got.exps.tolist() == want.exps
+        if ctype is int:
+            from paper_1303_7425_b200.parmul import limbs_to_ints
+            assert limbs_to_ints(got.coef, got.nl) == want.coeffs
+        else:
+            assert np.allclose(got.coef, np.asarray(want.coeffs), rtol=1e-12, atol=1e-9)
