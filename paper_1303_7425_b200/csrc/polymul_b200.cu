@@ -651,6 +651,8 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   const uint64_t span = (KH == ~0ull ? ((pb.P.kbits >= 64) ? ~0ull : ((1ull << pb.P.kbits) - 1))
                                      : KH - 1) - KL;
   if (span >= (1ull << 52)) return PGPU_OK;
+  // all-ones marks an empty hash slot: a record key may not take that value
+  if (sizeof(KT) == 4 && span >= 0xffffffffull) return PGPU_OK;
   uint32_t *rlo, *rhi;
   uint64_t* off;
   uint64_t chk;
