@@ -360,11 +360,10 @@ def main():
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
-        if r is not None:
+        if r is not None:  # same allocation pattern as the warm-up: free before the next step
             launches += r.launches
-            if last is not None:
-                last.free()
-            last = r
+            last = (r.n, r.nl, r.path)
+            r.free()
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -376,11 +375,7 @@ def main():
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
     value = total_pairs * args.steps / (total_ms / 1e3)
-    n_out = last.n if last is not None else 0
-    nl = last.nl if last is not None else 1
-    path_used = last.path if last is not None else "none"
-    if last is not None:
-        last.free()
+    n_out, nl, path_used = last if last is not None else (0, 1, "none")
 
     # dominant kernel from live CUDA events (phase timing on the launch stream)
     phase_runs = []

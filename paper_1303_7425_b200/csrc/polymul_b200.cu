@@ -419,8 +419,7 @@ int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint
                     uint64_t pairs, Slice* out) {
   out->n = 0;
   if (pairs == 0) return PGPU_OK;
-  uint64_t kmax_local = (KH == ~0ull ? ((pb.P.kbits >= 64) ? ~0ull : ((1ull << pb.P.kbits) - 1))
-                                     : KH - 1) - KL;
+  uint64_t kmax_local = std::min<uint64_t>(KH == ~0ull ? pb.kmax : KH - 1, pb.kmax) - KL;
   int bits = bitlen64(kmax_local);
   if (bits <= 32) return sort_range_rt<KT, uint32_t>(ctx, outer, pb, KL, KH, pairs, bits, out);
   return sort_range_rt<KT, uint64_t>(ctx, outer, pb, KL, KH, pairs, bits, out);
@@ -648,8 +647,8 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   // 2.4 ms vs 2.9 ms sorted).  At MP n=25 scale (2e9 pairs per batch) the
   // partial-sector writes run at ~0.3 TB/s and the radix sort wins.
   if (pairs > kBucketMaxPairs) return PGPU_OK;
-  const uint64_t span = (KH == ~0ull ? ((pb.P.kbits >= 64) ? ~0ull : ((1ull << pb.P.kbits) - 1))
-                                     : KH - 1) - KL;
+  // largest local key: the batch's upper bound, or the largest pair sum
+  const uint64_t span = std::min<uint64_t>(KH == ~0ull ? pb.kmax : KH - 1, pb.kmax) - KL;
   if (span >= (1ull << 52)) return PGPU_OK;
   // all-ones marks an empty hash slot: a record key may not take that value
   if (sizeof(KT) == 4 && span >= 0xffffffffull) return PGPU_OK;
@@ -702,6 +701,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   if (getenv("PGPU_DEBUG"))
     fprintf(stderr, "[pgpu] bucket range pairs=%llu span=%llu s1=%d coarse=%u fine=%u buckets=%u\n",
             (unsigned long long)pairs, (unsigned long long)span, s1, ncoarse, nbins, K);
+  ctx.tm.mark(1, "bins");
   // fill cursors start at the bin offsets (hist is reused)
   CUDA_TRY(cudaMemcpyAsync(hist, binoff, 4ull * nbins, cudaMemcpyDeviceToDevice, ctx.st));
   KT* rkey;
@@ -711,6 +711,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   k_bin_scatter<KT><<<wgrid, 256, 0, ctx.st>>>((const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, pb.na,
                                                KL, map, hist, rkey, rid);
   LAUNCHED(1);
+  ctx.tm.mark(2, "scatter");
   if (getenv("PGPU_DEBUG") && atoi(getenv("PGPU_DEBUG")) >= 2) {  // record invariants
     std::vector<KT> hk(pairs), ha(pb.na), hb(pb.nb);
     std::vector<uint64_t> hid(pairs);
@@ -736,7 +737,6 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
     }
     fprintf(stderr, "[pgpu] record check done (%d bad)\n", bad);
   }
-  ctx.tm.mark(1, "gen");
   const int nl = pb.nl ? pb.nl : 1;
   // staging holds every distinct term in the worst case (sparse products with
   // few collisions have almost as many terms as pairs); batches here are
