@@ -123,23 +123,36 @@ def power(base, n: int, mul, one):
 
 
 def evaluate(node, layout, ctype=int, mul=None):
+    """Value of an expression tree.  With the default (GPU) multiplier the
+    intermediate products of powering stay array-backed (ArrayPolynomial via
+    mul_arrays): no Python int is built until the final result."""
     if mul is None:
-        from .parmul import mul as gpu_mul
-        mul = gpu_mul
+        from .arrays import ArrayPolynomial
+        from .parmul import mul_arrays
+        out = _evaluate(node, layout, ctype, mul_arrays)
+        return out.to_poly() if isinstance(out, ArrayPolynomial) else out
+    return _evaluate(node, layout, ctype, mul)
+
+
+def _lists(p):
+    return p.to_poly() if hasattr(p, "to_poly") else p
+
+
+def _evaluate(node, layout, ctype, mul):
     kind = node[0]
     if kind == "num":
         return Polynomial.constant(layout, node[1], ctype)
     if kind == "var":
         return Polynomial.variable(layout, node[1], ctype)
     if kind == "pow":
-        base = evaluate(node[1], layout, ctype, mul)
+        base = _evaluate(node[1], layout, ctype, mul)
         return power(base, node[2], mul, Polynomial.constant(layout, 1, ctype))
-    left = evaluate(node[1], layout, ctype, mul)
-    right = evaluate(node[2], layout, ctype, mul)
+    left = _evaluate(node[1], layout, ctype, mul)
+    right = _evaluate(node[2], layout, ctype, mul)
     if kind == "add":
-        return left + right
+        return _lists(left) + _lists(right)
     if kind == "sub":
-        return left - right
+        return _lists(left) - _lists(right)
     return mul(left, right)
 
 
