@@ -93,7 +93,17 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
       for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x)
         reinterpret_cast<uint4*>(win)[q] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    for (uint32_t i = r0 + w; i < r1; i += nw) {
+    // every row spans the tile's whole column range (rlo is non-increasing in
+    // the row, rhi too): thread t owns column c0+t for all rows, so a mark is
+    // one broadcast shared load, an add and a byte store
+    const bool full = local && rlo[r0] <= c0 && rhi[r1 - 1] >= c1 && (c1 - c0) == (uint32_t)kSymCols &&
+                      blockDim.x == (unsigned)kSymCols;
+    if (full) {
+      const uint32_t boff = (uint32_t)((uint64_t)sb[threadIdx.x] - wlo);
+#pragma unroll 8
+      for (uint32_t i = 0; i < r1 - r0; ++i) win[(uint32_t)sa[i] + boff] = 1;
+    }
+    for (uint32_t i = r0 + w; !full && i < r1; i += nw) {
       const uint32_t lo = slo[i - r0], hi = shi[i - r0];
       const uint64_t ai = sa[i - r0];
       if (local) {
