@@ -56,6 +56,8 @@ def parse():
     ap.add_argument("--config", default="fateman30")
     ap.add_argument("--coeff", choices=["int", "float"], default="int")
     ap.add_argument("--path", default="auto")
+    ap.add_argument("--gather", default="peer", choices=("peer", "collective"),
+                    help="N>1: assemble the slices by peer copies (CUDA IPC) or an all-gather")
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -329,10 +331,22 @@ def main():
             else:
                 e = torch.zeros(0, dtype=torch.int64, device=dev)
                 c = torch.zeros((0, 3), dtype=torch.int64, device=dev)
-            gathered[0] = gather_slices(e, c)
+            if peer[0] is not None:
+                gathered[0] = peer[0].gather(e, c, stream=sptr)
+            else:
+                gathered[0] = gather_slices(e, c)
         return res
 
     gathered = [None]
+    # final gather of disjoint slices: peer copies over NVLink (CUDA IPC), or
+    # NCCL / gloo all-gather with --gather collective
+    peer = [None]
+    gather_kind = "none"
+    if world > 1:
+        gather_kind = args.gather
+        if args.gather == "peer":
+            from paper_1303_7425_b200.cluster import PeerGather
+            peer[0] = PeerGather(device=local)
 
     flush = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
@@ -436,6 +450,9 @@ def main():
                                          "accumulators proven wide enough (Fateman n=30: 136-bit)")
                           if args.coeff == "int" else "f64",
                           "parallelism": f"partition_by_ops x{world}" if world > 1 else "1 GPU",
+                          "gather": {"peer": "peer copies of disjoint slices (CUDA IPC, NVLink)",
+                                     "collective": "all-gather of disjoint slices",
+                                     "none": "none (1 GPU)"}[gather_kind],
                           "l2": f"flushed ({args.flush_mib} MiB write) between timed steps",
                           "plan_ms": plan_ms, "step_ms": [round(x, 3) for x in times]},
                "roofline": roof, "gpu_launches": launches, "clocks": ck}
@@ -475,6 +492,8 @@ def main():
                                "sample": desc, "seconds": dt}
     if out is not None:
         print(json.dumps(out), flush=True)
+    if peer[0] is not None:
+        peer[0].release()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

@@ -29,6 +29,11 @@
  *                       (io.py:241-248, io.py:306-308): the PolyFile text of a
  *                       product, formatted on the device
  *   pgpu_free_text      (ownership of the text; Python str in the reference)
+ *   pgpu_ipc_*          the final gather of paper Alg. 2 (cluster.py:365-379:
+ *                       nodes' disjoint results concatenated in rank order) as
+ *                       peer copies over NVLink: a shareable result buffer per
+ *                       rank, its CUDA IPC handle, and device-to-device copies
+ *                       of each rank's slice into every peer's buffer
  *
  * Every function returns a pgpu_status; on failure pgpu_last_error() holds a
  * message for the calling thread.  No function falls back to the CPU.
@@ -166,6 +171,18 @@ typedef struct pgpu_text {
 int pgpu_format(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64_t end,
                 const pgpu_options* opt, pgpu_text* out);
 void pgpu_free_text(pgpu_text* t);
+
+/* Peer buffers for the multi-GPU gather (one process per GPU).  A buffer from
+ * pgpu_ipc_alloc can be opened by another process with the 64-byte handle;
+ * pgpu_copy is an asynchronous device-to-device copy on `stream` (NULL: the
+ * library's stream of `device`), over NVLink when dst is a peer's buffer. */
+#define PGPU_IPC_HANDLE_BYTES 64
+int pgpu_ipc_alloc(int64_t bytes, int32_t device, void** dptr, void* handle);
+int pgpu_ipc_open(const void* handle, int32_t device, void** dptr);
+int pgpu_ipc_close(void* dptr);
+int pgpu_ipc_free(void* dptr);
+int pgpu_copy(void* dst, const void* src, int64_t bytes, int32_t device, void* stream);
+int pgpu_stream_sync(int32_t device, void* stream);
 
 const char* pgpu_last_error(void);
 int pgpu_device_count(void);

@@ -22,8 +22,10 @@ LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpolymul_b200.so"
 
 # Every symbol include/polymul_b200.h declares (checked by the CPU test suite).
 EXPORTS = ("pgpu_default_options", "pgpu_mul", "pgpu_count_below", "pgpu_free_result",
-           "pgpu_format", "pgpu_free_text", "pgpu_last_error", "pgpu_device_count",
+           "pgpu_format", "pgpu_free_text", "pgpu_ipc_alloc", "pgpu_ipc_open", "pgpu_ipc_close",
+           "pgpu_ipc_free", "pgpu_copy", "pgpu_stream_sync", "pgpu_last_error", "pgpu_device_count",
            "pgpu_abi_version")
+IPC_HANDLE_BYTES = 64
 
 
 class Layout(C.Structure):
@@ -92,6 +94,15 @@ def load(path: Path | None = None) -> C.CDLL:
         lib.pgpu_format.restype = C.c_int
         lib.pgpu_free_text.argtypes = [C.POINTER(Text)]
         lib.pgpu_free_text.restype = None
+        lib.pgpu_ipc_alloc.argtypes = [C.c_int64, C.c_int32, C.POINTER(C.c_void_p), C.c_void_p]
+        lib.pgpu_ipc_open.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_void_p)]
+        lib.pgpu_ipc_close.argtypes = [C.c_void_p]
+        lib.pgpu_ipc_free.argtypes = [C.c_void_p]
+        lib.pgpu_copy.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_int32, C.c_void_p]
+        lib.pgpu_stream_sync.argtypes = [C.c_int32, C.c_void_p]
+        for fn in ("pgpu_ipc_alloc", "pgpu_ipc_open", "pgpu_ipc_close", "pgpu_ipc_free", "pgpu_copy",
+                   "pgpu_stream_sync"):
+            getattr(lib, fn).restype = C.c_int
         lib.pgpu_last_error.argtypes = []
         lib.pgpu_last_error.restype = C.c_char_p
         lib.pgpu_device_count.argtypes = []

@@ -140,6 +140,91 @@ def gather_slices(exps, coef, group=None, device=None):
     return torch.cat(es), torch.cat(cs)
 
 
+class PeerGather:
+    """The final step of paper Alg. 2 as peer copies over NVLink (the north
+    star's "peer copies, no reduction collective"): every rank holds the
+    assembled product in a CUDA-IPC-shareable buffer whose handle the other
+    ranks open once; each rank then copies its own ordered slice straight into
+    every rank's buffer at its offset (device-to-device, through the peer
+    mapping), and a barrier marks all slices in place.  Buffers and peer
+    mappings are reused while the assembled size stays the same."""
+
+    def __init__(self, group=None, device: int = 0):
+        from . import _native as N
+        self.N, self.lib = N, N.load()
+        self.group, self.device = group, device
+        self.shape = None
+        self.bufs, self.dst = [], []
+
+    def _check(self, st):
+        if st != self.N.PGPU_OK:
+            raise self.N.NativeError(self.N.last_error())
+
+    def _setup(self, total: int, w: int):
+        import ctypes as C
+        import torch.distributed as dist
+        self.release()
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
+        handles = []
+        for nbytes in (total * 8, total * w * 8):
+            ptr, h = C.c_void_p(), C.create_string_buffer(self.N.IPC_HANDLE_BYTES)
+            self._check(self.lib.pgpu_ipc_alloc(nbytes, self.device, C.byref(ptr), h))
+            self.bufs.append(ptr.value)
+            handles.append(h.raw)
+        peers = _allgather_obj(handles, self.group)
+        self.dst = []
+        for r in range(world):
+            if r == rank:
+                self.dst.append((self.bufs[0], self.bufs[1], False))
+                continue
+            opened = []
+            for h in peers[r]:
+                ptr = C.c_void_p()
+                self._check(self.lib.pgpu_ipc_open(h, self.device, C.byref(ptr)))
+                opened.append(ptr.value)
+            self.dst.append((opened[0], opened[1], True))
+        self.shape = (total, w)
+
+    def gather(self, exps, coef, stream=None):
+        """(exps int64[total], coef int64[total, w]) views of the assembled product."""
+        import torch
+        import torch.distributed as dist
+        from .device import _CudaArray
+        rank = dist.get_rank(self.group)
+        n, w = int(exps.shape[0]), int(coef.shape[1])
+        counts = [int(x) for x in _allgather_obj(n, self.group)]
+        off = sum(counts[:rank])
+        total = sum(counts)
+        if self.shape != (total, w):
+            self._setup(total, w)
+        st = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        for de, dc, _ in self.dst:
+            self._check(self.lib.pgpu_copy(de + off * 8, exps.data_ptr(), n * 8, self.device, st))
+            self._check(self.lib.pgpu_copy(dc + off * w * 8, coef.data_ptr(), n * w * 8, self.device, st))
+        self._check(self.lib.pgpu_stream_sync(self.device, st))
+        dist.barrier(self.group)  # every rank's slice is in every buffer
+        dev = torch.device("cuda", self.device)
+        if total == 0:
+            return torch.zeros(0, dtype=torch.int64, device=dev), torch.zeros((0, w), dtype=torch.int64, device=dev)
+        return (torch.as_tensor(_CudaArray(self.bufs[0], (total,), "<i8"), device=dev),
+                torch.as_tensor(_CudaArray(self.bufs[1], (total, w), "<i8"), device=dev))
+
+    def release(self):
+        """Unmap the peers' buffers and free ours (collective: call on every rank)."""
+        import torch.distributed as dist
+        if not self.bufs:
+            return
+        dist.barrier(self.group)  # nobody still writes into our buffers
+        for de, dc, opened in self.dst:
+            if opened:
+                self.lib.pgpu_ipc_close(de)
+                self.lib.pgpu_ipc_close(dc)
+        dist.barrier(self.group)  # peers unmapped before the memory goes away
+        for ptr in self.bufs:
+            self.lib.pgpu_ipc_free(ptr)
+        self.bufs, self.dst, self.shape = [], [], None
+
+
 def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
     """Distributed product; every rank returns the full Polynomial.
 

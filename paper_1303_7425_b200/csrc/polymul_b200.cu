@@ -1368,6 +1368,61 @@ void pgpu_free_text(pgpu_text* t) {
   t->bytes = 0;
 }
 
+int pgpu_ipc_alloc(int64_t bytes, int32_t device, void** dptr, void* handle) {
+  if (!dptr || !handle || bytes < 0) return fail(PGPU_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  *dptr = nullptr;
+  // plain cudaMalloc: stream-ordered pool memory is not IPC-shareable by default
+  CUDA_TRY(cudaMalloc(dptr, (size_t)std::max<int64_t>(bytes, 256)));
+  cudaIpcMemHandle_t h;
+  cudaError_t e = cudaIpcGetMemHandle(&h, *dptr);
+  if (e != cudaSuccess) {
+    cudaFree(*dptr);
+    *dptr = nullptr;
+    return fail(PGPU_ECUDA, "cudaIpcGetMemHandle failed: %s", cudaGetErrorString(e));
+  }
+  static_assert(sizeof(h) <= PGPU_IPC_HANDLE_BYTES, "IPC handle size");
+  memset(handle, 0, PGPU_IPC_HANDLE_BYTES);
+  memcpy(handle, &h, sizeof h);
+  return PGPU_OK;
+}
+
+int pgpu_ipc_open(const void* handle, int32_t device, void** dptr) {
+  if (!dptr || !handle) return fail(PGPU_EINVAL, "null argument");
+  CUDA_TRY(cudaSetDevice(device));
+  cudaIpcMemHandle_t h;
+  memcpy(&h, handle, sizeof h);
+  CUDA_TRY(cudaIpcOpenMemHandle(dptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return PGPU_OK;
+}
+
+int pgpu_ipc_close(void* dptr) {
+  CUDA_TRY(cudaIpcCloseMemHandle(dptr));
+  return PGPU_OK;
+}
+
+int pgpu_ipc_free(void* dptr) {
+  CUDA_TRY(cudaFree(dptr));
+  return PGPU_OK;
+}
+
+int pgpu_copy(void* dst, const void* src, int64_t bytes, int32_t device, void* stream) {
+  if (bytes <= 0) return PGPU_OK;
+  if (!dst || !src) return fail(PGPU_EINVAL, "null argument");
+  cudaStream_t lib_st;
+  TRY(device_setup(device, &lib_st));
+  CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
+                           stream ? (cudaStream_t)stream : lib_st));
+  return PGPU_OK;
+}
+
+int pgpu_stream_sync(int32_t device, void* stream) {
+  cudaStream_t lib_st;
+  TRY(device_setup(device, &lib_st));
+  CUDA_TRY(cudaStreamSynchronize(stream ? (cudaStream_t)stream : lib_st));
+  return PGPU_OK;
+}
+
 const char* pgpu_last_error(void) { return g_err.c_str(); }
 
 int pgpu_device_count(void) {

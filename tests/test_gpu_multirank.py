@@ -1,5 +1,6 @@
 """The N>1 bench path (paper Alg. 2: partition_by_ops ranges, per-rank GPU
-range products, rank-ordered all-gather) run as 2 and 3 torchrun ranks that
+range products, the rank-ordered gather by peer copies through CUDA IPC or by
+an all-gather) run as 2 and 3 torchrun ranks that
 share cuda:0 over gloo; the assembled product must carry the reference digest.
 (The real N-GPU run uses NCCL; only one GPU is available to the tests.)"""
 
@@ -25,12 +26,14 @@ def _port():
     return p
 
 
-@pytest.mark.parametrize("ranks,config", [(2, "fateman10"), (3, "fateman20"), (2, "mp12")])
-def test_emulated_ranks_reproduce_reference_digest(ranks, config):
+@pytest.mark.parametrize("ranks,config,gather", [(2, "fateman10", "peer"), (3, "fateman20", "peer"),
+                                                 (2, "mp12", "peer"), (2, "fateman10", "collective"),
+                                                 (3, "mp12", "collective")])
+def test_emulated_ranks_reproduce_reference_digest(ranks, config, gather):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"),
            "--gpus", str(ranks), "--config", config, "--steps", "1", "--warmup", "1",
-           "--emulate-ranks", "--verify"]
+           "--emulate-ranks", "--verify", "--gather", gather]
     out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
     assert out.returncode == 0, out.stderr[-2000:]
     lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
