@@ -247,6 +247,7 @@ def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
     if count_fn is None:
         def count_fn(x, y, bnd):
             return parmul.count_below(x, y, bnd, device=cfg.device)
+    device_path = local_fn is None and world > 1
     if local_fn is None:
         def local_fn(x, y, lo, hi):
             return parmul.native_mul(parmul.Operand.from_poly(x), parmul.Operand.from_poly(y),
@@ -254,6 +255,8 @@ def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
                                      float_ordered=cfg.float_ordered, device=cfg.device)
     bounds, plan = plan_for_ranks(a, b, cfg.l, world, rank, count_fn, group)
     lo, hi = rank_range(bounds, plan, rank)
+    if device_path:
+        return _gpu_range_and_peer_gather(a, b, cfg, lo, hi, group)
     if lo < hi:
         raw = local_fn(a, b, lo, hi)
     else:
@@ -300,3 +303,53 @@ def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
         nl = wd
     raw_all = parmul.RawProduct(exps, coef, nkind, nl, 0, "", 0, 0, {})
     return parmul.to_poly(cls, a.layout, a.ctype, raw_all)
+
+
+def _gpu_range_and_peer_gather(a, b, cfg, lo, hi, group):
+    """One rank's range product left on its GPU, then the peer-copy gather
+    (PeerGather) and a single device-to-host copy of the assembled product."""
+    import numpy as np
+    import torch
+    from . import parmul
+    from .device import DeviceOperand, mul_on_device
+    cls = type(a)
+    dev = torch.device("cuda", cfg.device)
+    res = None
+    if lo < hi:
+        dA = DeviceOperand(parmul.Operand.from_poly(a), dev)
+        dB = DeviceOperand(parmul.Operand.from_poly(b), dev)
+        res = mul_on_device(dA, dB, a.layout, lo=lo, hi=hi, path=cfg.path,
+                            float_ordered=cfg.float_ordered, device=cfg.device)
+    try:
+        if res is not None and res.n:
+            e, c = res.tensors()
+            c = c.view(torch.int64).reshape(e.shape[0], -1)
+            kind = (res.kind, res.nl)
+        else:
+            e = torch.zeros(0, dtype=torch.int64, device=dev)
+            c = torch.zeros((0, 1), dtype=torch.int64, device=dev)
+            kind = None
+        kinds = _allgather_obj((kind, int(c.shape[1])), group)
+        wd = max(k[1] for k in kinds)
+        kind = next((k[0] for k in kinds if k[0] is not None), None)
+        if c.shape[1] < wd:  # sign-extend narrower limb sets (exact ints)
+            sign = (c[:, -1:] >> 63).expand(-1, wd - c.shape[1])
+            c = torch.cat([c, sign], dim=1)
+        pg = PeerGather(group, cfg.device)
+        try:
+            ge, gc = pg.gather(e.contiguous(), c.contiguous())
+            exps = ge.cpu().numpy().view(np.uint64)
+            words = gc.cpu().numpy().view(np.uint64)
+        finally:
+            pg.release()
+    finally:
+        if res is not None:
+            res.free()
+    if kind is None:
+        return cls.zero(a.layout, a.ctype)
+    nkind, nl = kind
+    if a.ctype is float:
+        coef = words.reshape(-1).view(np.float64)
+    else:
+        coef, nl = words, wd
+    return parmul.to_poly(cls, a.layout, a.ctype, parmul.RawProduct(exps, coef, nkind, nl, 0, "", 0, 0, {}))

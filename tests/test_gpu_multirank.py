@@ -40,3 +40,17 @@ def test_emulated_ranks_reproduce_reference_digest(ranks, config, gather):
     assert len(lines) == 1
     v = lines[0]["verified"]
     assert v["ok"], v
+
+
+@pytest.mark.parametrize("ranks,cfg", [(2, "fateman10/int"), (3, "mp12/int"), (2, "fateman10/float")])
+def test_gpu_mul_api_peer_gather(ranks, cfg):
+    """cluster.gpu_mul (the multi-GPU public API) over emulated ranks: range
+    products on the GPU, peer-copy gather, reference digest."""
+    from conftest import digests
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
+           "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "tests" / "multirank_api.py"), cfg]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    got = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")][0]
+    want = digests()["products"][cfg]
+    assert got["n"] == want["n"] and got["sha256"] == want["sha256"] and got["type"] == "Polynomial"
