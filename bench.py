@@ -87,7 +87,7 @@ class NvmlClocks:
     REASONS = {"hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40,
                "sw_power_cap": 0x4}
 
-    def __init__(self, index: int, period_s: float = 0.25):
+    def __init__(self, index: int, period_s: float = 0.01):
         self.index = index
         self.period = period_s
         self.samples = []

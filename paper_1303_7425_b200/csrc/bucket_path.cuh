@@ -40,7 +40,10 @@ namespace pgpu {
 constexpr int kBucketCap = PGPU_BUCKET_CAP;  // pairs per bucket (max)
 constexpr int kBucketHalf = kBucketCap / 2;
 constexpr int kBucketTable = 2 * kBucketCap; // hash slots (load factor <= 1/2)
-constexpr int kBucketThreads = 256;
+#ifndef PGPU_BUCKET_THREADS
+#define PGPU_BUCKET_THREADS 256
+#endif
+constexpr int kBucketThreads = PGPU_BUCKET_THREADS;
 
 // ---- B1 / B3: walk of a batch's pairs ----------------------------------------
 // One warp per row, lanes on consecutive columns (as k_gen).  For each group of
