@@ -476,15 +476,10 @@ k_bucket_gather(const uint64_t* __restrict__ bbase, const uint32_t* __restrict__
     ocoef[dst * nl + t] = scoef[src * nl + t];
 }
 
-// bin offsets; flags a bin too large for the bucket bound (then the batch
-// takes the sort path)
+// bin offsets (exclusive scan of the fine-bin histogram)
 struct BinOffOut {
   uint32_t* binoff;
-  uint32_t* big;
-  __device__ void operator()(uint64_t b, uint32_t ex, uint32_t v) const {
-    binoff[b] = ex;
-    if (v > (uint32_t)kBucketHalf) *big = 1u;
-  }
+  __device__ void operator()(uint64_t b, uint32_t ex, uint32_t) const { binoff[b] = ex; }
 };
 struct HistGen {
   const uint32_t* hist;

@@ -689,7 +689,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   k_bin_count<KT><<<wgrid, 256, 0, ctx.st>>>((const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, pb.na,
                                              KL, map, hist);
   LAUNCHED(1);
-  LAUNCHED(device_scan<uint32_t>(nbins, HistGen{hist}, BinOffOut{binoff, flags}, part, &g, ctx.st));
+  LAUNCHED(device_scan<uint32_t>(nbins, HistGen{hist}, BinOffOut{binoff}, part, &g, ctx.st));
   // buckets (BStartGen): runs of small bins, big bins on their own
   uint32_t* bstart;
   TRY(ctx.ar->alloc(&bstart, (size_t)nbins + 1));
