@@ -196,7 +196,11 @@ constexpr int kNumThreads = kNumWarps * 32;
 constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot table
 constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
 constexpr size_t kAccBytes = 80 * 1024;
-constexpr int kUnroll = PGPU_UNROLL;           // independent columns per lane per step
+constexpr int kUnroll = PGPU_UNROLL;       // independent columns per lane per step
+#ifndef PGPU_ROW_CLAIM
+#define PGPU_ROW_CLAIM 32
+#endif
+constexpr int kRowClaim = PGPU_ROW_CLAIM;  // rows a warp claims at a time (<= 32; 32 measured best)
 
 // Accumulator geometry.  NW = words of a finished term.  CB = 1: the term is
 // held as 4 word planes plus a one-byte carry counter (nonnegative products
@@ -486,11 +490,11 @@ k_numeric(NumArgs A) {
       // warps claim 32-row groups dynamically (one shared counter per interval)
       for (;;) {
         uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(&row_ctr, 32u);
+        if (lane == 0) g = atomicAdd(&row_ctr, (uint32_t)kRowClaim);
         g = rb0 + __shfl_sync(0xffffffffu, g, 0);
         if (g >= rb1) break;
         const uint32_t i = g + lane;
-        const bool rowok = i < rb1;
+        const bool rowok = lane < kRowClaim && i < rb1;
         uint32_t ci = rowok ? cur[i] : 0u;
         KT nki = rowok ? nk[i] : kInf;
         unsigned todo = __ballot_sync(0xffffffffu, (uint64_t)nki < Khi);
