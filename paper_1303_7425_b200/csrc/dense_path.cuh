@@ -238,6 +238,7 @@ struct NumArgs {
   uint64_t* oexp;
   uint64_t* ocoef;
   uint32_t* onz;
+  uint32_t* unit_ctr;  // persistent CTAs: next unit to claim (zeroed before launch)
 };
 
 // Finished term: NW words -> nl sign-extended u64 limbs + nonzero flag.
@@ -318,8 +319,7 @@ __device__ __forceinline__ uint32_t rank_of(uint64_t klocal, const uint32_t* __r
 // is >= the current interval's lower bound), so a row's run in interval t is
 // found by walking forward from its cursor -- no per-interval edge search.
 template <typename KT, int NW, int MODE, int CB>
-__global__ void __launch_bounds__(kNumThreads)
-k_numeric(NumArgs A) {
+__device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t unit) {
   using G = Geo<NW, CB>;
   constexpr uint32_t D = G::D;
   constexpr uint32_t DP = G::DP;
@@ -333,7 +333,7 @@ k_numeric(NumArgs A) {
   const KT* __restrict__ ak = (const KT*)A.ak;
   const KT* __restrict__ bk = (const KT*)A.bk;
   const KT* __restrict__ okey = (const KT*)A.okey;
-  const uint32_t r = blockIdx.x % A.R, s = blockIdx.x / A.R;
+  const uint32_t r = unit % A.R, s = unit / A.R;
   const uint32_t t_begin = (uint32_t)((uint64_t)A.T * s / A.S);
   const uint32_t t_end = (uint32_t)((uint64_t)A.T * (s + 1) / A.S);
   const uint32_t rb0 = (uint32_t)((uint64_t)A.na * r / A.R);
@@ -583,6 +583,30 @@ k_numeric(NumArgs A) {
     }
     __syncthreads();
   }
+}
+
+// Persistent CTAs (one per resident slot) claim (row block, segment) units in
+// key order from a counter: no partial last wave, and the light units at the
+// top of the key range finish the grid.
+#ifndef PGPU_PERSISTENT
+#define PGPU_PERSISTENT 1
+#endif
+template <typename KT, int NW, int MODE, int CB>
+__global__ void __launch_bounds__(kNumThreads)
+k_numeric(NumArgs A) {
+#if PGPU_PERSISTENT
+  __shared__ uint32_t unit_s;
+  for (;;) {
+    if (threadIdx.x == 0) unit_s = atomicAdd(A.unit_ctr, 1u);
+    __syncthreads();
+    const uint32_t unit = unit_s;
+    __syncthreads();
+    if (unit >= A.R * A.S) return;
+    numeric_unit<KT, NW, MODE, CB>(A, unit);
+  }
+#else
+  numeric_unit<KT, NW, MODE, CB>(A, blockIdx.x);
+#endif
 }
 
 // ---- D5 ---------------------------------------------------------------------
