@@ -409,12 +409,12 @@ def main():
     out = None
     if rank == 0:
         peak, peak_src = hbm_peak()
-        if "numeric" in phases:
-            kern = "numeric"
-        elif path_used == "bucket" and "reduce" in phases:
-            kern = "reduce"
-        else:
-            kern = "sort" if "sort" in phases else None
+        # dominant kernel phase: dense numeric pass, radix sort, or bucket reduce
+        # (a product can mix bucket and sort batches)
+        cands = {k: phases[k] for k in ("numeric", "sort", "reduce") if k in phases}
+        kern = max(cands, key=cands.get) if cands else None
+        if kern == "reduce" and path_used != "bucket":
+            kern = "sort" if "sort" in phases else kern
         kern_ms = phases.get(kern, float("nan")) if kern else float("nan")
         w_c = 8 if args.coeff == "float" else 8 * nl
         w_in = 8 if A.kind != 2 else 16
@@ -428,7 +428,8 @@ def main():
                 traffic = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
             except Exception:
                 traffic = None
-        kname = {"numeric": f"k_numeric ({path_used} path)", "reduce": "k_bucket_reduce (bucket path)",
+        kname = {"numeric": f"k_numeric ({path_used} path)",
+                 "reduce": "k_bucket_reduce (bucket path)" if path_used == "bucket" else "k_seg_reduce (sort path)",
                  "sort": "k_rs_onesweep passes (sort path)"}.get(kern, kern)
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
