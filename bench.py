@@ -411,10 +411,8 @@ def main():
         peak, peak_src = hbm_peak()
         # dominant kernel phase: dense numeric pass, radix sort, or bucket reduce
         # (a product can mix bucket and sort batches)
-        cands = {k: phases[k] for k in ("numeric", "sort", "reduce") if k in phases}
+        cands = {k: phases[k] for k in ("numeric", "sort", "reduce", "bucket_reduce") if k in phases}
         kern = max(cands, key=cands.get) if cands else None
-        if kern == "reduce" and path_used != "bucket":
-            kern = "sort" if "sort" in phases else kern
         kern_ms = phases.get(kern, float("nan")) if kern else float("nan")
         w_c = 8 if args.coeff == "float" else 8 * nl
         w_in = 8 if A.kind != 2 else 16
@@ -429,7 +427,7 @@ def main():
             except Exception:
                 traffic = None
         kname = {"numeric": f"k_numeric ({path_used} path)",
-                 "reduce": "k_bucket_reduce (bucket path)" if path_used == "bucket" else "k_seg_reduce (sort path)",
+                 "bucket_reduce": "k_bucket_reduce (bucket path)", "reduce": "k_seg_reduce (sort path)",
                  "sort": "k_rs_onesweep passes (sort path)"}.get(kern, kern)
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",

@@ -701,7 +701,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   if (getenv("PGPU_DEBUG"))
     fprintf(stderr, "[pgpu] bucket range pairs=%llu span=%llu s1=%d coarse=%u fine=%u buckets=%u\n",
             (unsigned long long)pairs, (unsigned long long)span, s1, ncoarse, nbins, K);
-  ctx.tm.mark(1, "bins");
+  ctx.tm.mark(6, "bucket_bins");
   // fill cursors start at the bin offsets (hist is reused)
   CUDA_TRY(cudaMemcpyAsync(hist, binoff, 4ull * nbins, cudaMemcpyDeviceToDevice, ctx.st));
   KT* rkey;
@@ -711,7 +711,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   k_bin_scatter<KT><<<wgrid, 256, 0, ctx.st>>>((const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, pb.na,
                                                KL, map, hist, rkey, rid);
   LAUNCHED(1);
-  ctx.tm.mark(2, "scatter");
+  ctx.tm.mark(6, "bucket_bins");
   if (getenv("PGPU_DEBUG") && atoi(getenv("PGPU_DEBUG")) >= 2) {  // record invariants
     std::vector<KT> hk(pairs), ha(pb.na), hb(pb.nb);
     std::vector<uint64_t> hid(pairs);
@@ -784,7 +784,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   }
   LAUNCHED(1);
   CUDA_TRY(cudaGetLastError());
-  ctx.tm.mark(3, "reduce");
+  ctx.tm.mark(7, "bucket_reduce");
   unsigned long long nnz;
   uint32_t ovf;
   CUDA_TRY(cudaMemcpyAsync(&nnz, sctr, 8, cudaMemcpyDeviceToHost, ctx.st));
