@@ -491,15 +491,33 @@ int sort_range_rt(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64
                                                 (const double*)pb.bcoef, KL, pb.P, sexp,
                                                 (double*)scoef, snz);
   } else {
-#define SEGRED(NL_, CK_)                                                                   \
-  k_seg_reduce_int<RT, NL_, CK_><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, pb.acoef, \
-                                                         pb.bcoef, KL, pb.P, sexp, scoef, snz)
+    // lanes per segment from the mean segment length (about 16-24 pairs per lane)
+    const uint64_t mean = pairs / std::max<uint32_t>(nseg, 1);
+    int G = 1;
+    while (G < 32 && (uint64_t)G * 24 < mean) G <<= 1;  // MP n=25 (mean 65): G = 4, measured best
+    if (const char* e = getenv("PGPU_SEG_LANES")) G = atoi(e);
+    const int grg = grid_for((int64_t)nseg * G, 256, 1 << 30);
+#define SEGRED_G(NL_, CK_, G_)                                                                    \
+  k_seg_reduce_int<RT, NL_, CK_, G_><<<grg, 256, 0, ctx.st>>>(keys, vals, starts, nseg, pb.acoef, \
+                                                              pb.bcoef, KL, pb.P, sexp, scoef, snz)
+#define SEGRED(NL_, CK_)                         \
+  do {                                           \
+    switch (G) {                                 \
+      case 1: SEGRED_G(NL_, CK_, 1); break;      \
+      case 2: SEGRED_G(NL_, CK_, 2); break;      \
+      case 4: SEGRED_G(NL_, CK_, 4); break;      \
+      case 8: SEGRED_G(NL_, CK_, 8); break;      \
+      case 16: SEGRED_G(NL_, CK_, 16); break;    \
+      default: SEGRED_G(NL_, CK_, 32); break;    \
+    }                                            \
+  } while (0)
     if (pb.ck == PGPU_I64) {
       if (nl == 1) SEGRED(1, 1); else if (nl == 2) SEGRED(2, 1); else SEGRED(3, 1);
     } else {
       if (nl == 1) SEGRED(1, 2); else if (nl == 2) SEGRED(2, 2); else SEGRED(3, 2);
     }
 #undef SEGRED
+#undef SEGRED_G
   }
   LAUNCHED(1);
   ctx.tm.mark(3, "reduce");

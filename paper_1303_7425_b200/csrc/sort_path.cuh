@@ -246,23 +246,39 @@ struct HeadOut {
 };
 
 // ---- K4: segment reduce (one owner per output term) -------------------------
-template <typename KT, int NL, int CK>
+// G lanes own one segment (G = 1, 2, ..., 32, picked from the mean segment
+// length): they stride over its pairs with coalesced record loads, then fold
+// their exact partial sums with shuffles (limb adds modulo 2^(64 NL); the
+// proven bound keeps the sum below 2^(64 NL - 1)).  Integer sums are
+// order-independent, so any G gives the same result.
+template <typename KT, int NL, int CK, int G>
 __global__ void __launch_bounds__(256)
 k_seg_reduce_int(const KT* __restrict__ keys, const uint64_t* __restrict__ vals,
                  const uint32_t* __restrict__ starts, uint32_t nseg, const void* __restrict__ ac,
                  const void* __restrict__ bc, uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp,
                  uint64_t* __restrict__ ocoef, uint32_t* __restrict__ onz) {
-  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= nseg) return;
-  uint32_t p0 = starts[s], p1 = starts[s + 1];
+  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint32_t g = threadIdx.x % G;
+  const bool live = s < nseg;  // whole groups are live or not; every lane reaches the shuffles
+  const uint32_t p0 = live ? starts[s] : 0u, p1 = live ? starts[s + 1] : 0u;
   Limbs<NL> acc;
   limbs_zero(acc);
-  for (uint32_t p = p0; p < p1; ++p) {
+  for (uint32_t p = p0 + g; p < p1; p += G) {
     uint64_t v = vals[p];
     ICoef a = load_icoef<CK>(ac, (int64_t)(v >> 32));
     ICoef b = load_icoef<CK>(bc, (int64_t)(v & 0xffffffffu));
     limbs_add(acc, imul<NL, CK>(a, b));
   }
+  if constexpr (G > 1) {
+#pragma unroll
+    for (int d = G / 2; d >= 1; d >>= 1) {
+      Limbs<NL> o;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) o.w[k] = __shfl_down_sync(0xffffffffu, acc.w[k], d, G);
+      limbs_add(acc, o);
+    }
+  }
+  if (!live || g != 0) return;
   oexp[s] = expand_key((uint64_t)keys[p0] + KL, P);
 #pragma unroll
   for (int k = 0; k < NL; ++k) ocoef[(uint64_t)s * NL + k] = acc.w[k];
