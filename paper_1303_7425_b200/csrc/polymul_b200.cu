@@ -680,7 +680,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   const uint64_t target = std::max<uint64_t>(1, std::min<uint64_t>(pairs / 16, 1ull << 22));
   const int s1 = std::max(0, bitlen64(span) - bitlen64(target - 1));
   const uint32_t ncoarse = (uint32_t)((span >> s1) + 1);
-  uint32_t *hist1, *tab, *flags;
+  uint32_t *hist1, *tab, *flags;  // flags[1]: the reduce kernel's fallback flag
   TRY(ctx.ar->alloc(&hist1, ncoarse));
   TRY(ctx.ar->alloc(&tab, ncoarse));
   TRY(ctx.ar->alloc(&flags, 4));
@@ -811,7 +811,7 @@ int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, ui
   if (getenv("PGPU_DEBUG"))
     fprintf(stderr, "[pgpu] bucket terms=%llu staging=%llu overflow=%u\n", nnz,
             (unsigned long long)scap, ovf);
-  if (ovf) return PGPU_OK;  // more terms than the staging estimate
+  if (ovf) return PGPU_OK;  // a large bin's key window exceeds the table: sort path
   uint64_t* boff;
   uint64_t* part64;
   TRY(ctx.ar->alloc(&boff, K));
