@@ -8,9 +8,13 @@ library (lib/libpolymul_b200.so); there is no CPU fallback.
 """
 
 from .core import (SENTINEL, CoefficientOverflowError, ExponentOverflowError, Layout, Polynomial,
-                   VarTable, canonicalize, check_product_fits, default_layout)
+                   VarTable, canonicalize, check_product_fits, default_layout, naive_mul)
 from .arrays import ArrayPolynomial
-from .io import format_poly, format_text, poly_digest, text_digest, write_poly
+from .io import (PolyIOError, format_poly, format_text, parse_poly, poly_digest, read_poly, text_digest,
+                 write_poly)
+from .expr import ExprSyntaxError, poly_from_expr
+from .expr import evaluate as eval_expr
+from .expr import parse as parse_expr
 from .parmul import MulConfig, count_below, mul, mul_arrays, native_mul
 from .split import GridParams, SplitSet, select_grid
 from .cluster import ClusterPlan, gpu_mul, partition_by_ops
@@ -19,7 +23,9 @@ __version__ = "0.1.0"
 
 __all__ = [
     "SENTINEL", "CoefficientOverflowError", "ExponentOverflowError", "Layout", "Polynomial",
-    "VarTable", "canonicalize", "check_product_fits", "default_layout", "format_poly",
+    "VarTable", "canonicalize", "check_product_fits", "default_layout", "naive_mul", "format_poly",
+    "PolyIOError", "parse_poly", "read_poly", "ExprSyntaxError", "poly_from_expr", "eval_expr",
+    "parse_expr",
     "poly_digest", "ArrayPolynomial", "format_text", "text_digest", "write_poly", "MulConfig",
     "count_below", "mul", "mul_arrays", "native_mul", "GridParams", "SplitSet",
     "select_grid", "ClusterPlan", "gpu_mul", "partition_by_ops", "__version__",

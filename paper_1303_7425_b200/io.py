@@ -20,6 +20,64 @@ import numpy as np
 from . import _native as N
 
 DEFAULT_CHUNK_TERMS = 1 << 22
+_FLOAT_MARKS = (".", "e", "E", "n", "i")  # decimals, exponents, nan/inf
+
+
+class PolyIOError(ValueError):
+    """Malformed polynomial file; the message names the offending line
+    (reference io.py:34-35)."""
+
+
+def parse_poly(text: str, layout=None, ctype=None):
+    """PolyFile text -> Polynomial (reference io.py:251-290, same rules and
+    messages): a `vars` header, then `coeff e1 ... em` lines; '#' comments and
+    blank lines skipped; duplicate exponents combined; ctype inferred from the
+    coefficient spelling unless given.  Host-side input parsing (operands)."""
+    from .core import Polynomial, VarTable, default_layout
+    vars_decl = None
+    raw = []
+    for lineno, line in enumerate(text.splitlines(), start=1):
+        st = line.strip()
+        if not st or st.startswith("#"):
+            continue
+        fields = st.split()
+        if vars_decl is None:
+            if fields[0] != "vars" or len(fields) < 2:
+                raise PolyIOError(f"line {lineno}: expected 'vars <name>...' header")
+            try:
+                vars_decl = VarTable(tuple(fields[1:]))
+            except ValueError as exc:
+                raise PolyIOError(f"line {lineno}: {exc}") from None
+            continue
+        raw.append((lineno, fields))
+    if vars_decl is None:
+        raise PolyIOError("missing 'vars' header line")
+    if layout is None:
+        layout = default_layout(vars_decl.names)
+    elif tuple(layout.vars.names) != tuple(vars_decl.names):
+        raise PolyIOError(f"file declares variables {vars_decl.names}, expected {layout.vars.names}")
+    if ctype is None:
+        ctype = float if any(any(m in f[0] for m in _FLOAT_MARKS) for _, f in raw) else int
+    terms = []
+    for lineno, fields in raw:
+        if len(fields) != 1 + vars_decl.m:
+            raise PolyIOError(f"line {lineno}: expected coefficient plus {vars_decl.m} exponents, "
+                              f"got {len(fields)} fields")
+        try:
+            coeff = ctype(fields[0])
+            vec = tuple(int(f) for f in fields[1:])
+        except ValueError:
+            raise PolyIOError(f"line {lineno}: malformed number") from None
+        if any(v < 0 for v in vec):
+            raise PolyIOError(f"line {lineno}: negative exponent")
+        terms.append((coeff, vec))
+    return Polynomial(layout, terms, ctype)
+
+
+def read_poly(path, layout=None, ctype=None):
+    """reference io.read_poly (io.py:301-303)."""
+    with open(path, "r", encoding="utf-8") as fh:
+        return parse_poly(fh.read(), layout, ctype)
 
 
 def format_poly(poly) -> str:

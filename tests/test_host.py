@@ -166,3 +166,26 @@ def test_limb_marshaling_helper_matches_python_ints():
         vals = [v for v in vals if -2 ** (B - 1) <= v < 2 ** (B - 1)]
         arr, _ = int_limbs(vals, nl)
         assert parmul.limbs_to_ints(arr, nl) == vals
+
+
+def test_polyfile_reader_mirrors_reference_rules():
+    """parse_poly (reference io.py:251-290): round trip of format_poly, ctype
+    inference, duplicate lines combined, and the reference's error messages."""
+    from paper_1303_7425_b200 import PolyIOError, format_poly, parse_poly
+    from conftest import golden_cases
+    for _, a, b, _, _ in golden_cases()[::9]:
+        for p in (a, b):
+            q = parse_poly(format_poly(p), p.layout)
+            assert q.exps == p.exps and q.ctype is p.ctype
+            assert [repr(c) for c in q.coeffs] == [repr(c) for c in p.coeffs]
+    p = parse_poly("# c\nvars x y\n2 1 0\n3 1 0\n-5 0 0\n")
+    assert p.ctype is int and p.n == 2 and p.coeffs == [-5, 5]
+    assert parse_poly("vars x\n1.5 2\n").ctype is float
+    for text, msg in [("1 2\n", "line 1: expected 'vars <name>...' header"),
+                      ("", "missing 'vars' header line"),
+                      ("vars x\n1 2 3\n", "line 2: expected coefficient plus 1 exponents, got 3 fields"),
+                      ("vars x\n1 -2\n", "line 2: negative exponent"),
+                      ("vars x\nq 2\n", "line 2: malformed number")]:
+        with pytest.raises(PolyIOError) as exc:
+            parse_poly(text)
+        assert str(exc.value) == msg
