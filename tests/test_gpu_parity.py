@@ -335,3 +335,33 @@ def test_bucket_path_random_sparse_vs_oracle(ctype, rng):
             assert limbs_to_ints(got.coef, got.nl) == want.coeffs
         else:
             assert np.allclose(got.coef, np.asarray(want.coeffs), rtol=1e-12, atol=1e-9)
+
+
+@pytest.mark.parametrize("path", ["auto", "dense", "bucket", "sort"])
+def test_degenerate_shapes_and_field_limits(path):
+    """1xN, Nx1 and 1x1 products, exponents exactly at the field caps (the
+    reference's overflow test is componentwise max <= cap, core.py:365-385),
+    and a one-variable lex layout with a 63-bit field, on every path."""
+    from paper_1303_7425_b200.core import Layout, VarTable, naive_mul
+    lay = default_layout(("x", "y", "z"))
+    big = Polynomial(lay, [(k + 1, (k % 7, k % 5, k % 3)) for k in range(300)], int)
+    one = Polynomial(lay, [(-3, (2, 0, 1))], int)
+    cases = [(big, one), (one, big), (one, one)]
+    m = lay.max_total_degree() // 2  # products reach the degree cap exactly
+    hi = Polynomial(lay, [(5, (m, 0, 0)), (7, (0, m, 0))], int)
+    lo = Polynomial(lay, [(2, (0, 0, 0)), (1, (m, 0, 0)), (-4, (0, 0, m))], int)
+    cases.append((hi, lo))
+    lex1 = Layout(VarTable(("x",)), "lex", (63,))
+    a = Polynomial(lex1, [(1, (0,)), (2, (1 << 40,)), (3, (1 << 61,))], int)
+    b = Polynomial(lex1, [(4, (5,)), (-5, (1 << 60,))], int)
+    cases.append((a, b))
+    for f, g in cases:
+        try:
+            got = mul(f, g, MulConfig(path=path))
+        except Exception as exc:  # the dense path refuses key spans it cannot map
+            assert path == "dense" and "dense path" in str(exc)
+            continue
+        want = naive_mul(f, g)
+        assert got.exps == want.exps and got.coeffs == want.coeffs
+    with pytest.raises(ExponentOverflowError):
+        mul(hi, Polynomial(lay, [(1, (m + 1, 0, 0))], int), MulConfig(path=path))
