@@ -75,9 +75,12 @@ typedef enum pgpu_path {
   PGPU_PATH_AUTO = 0,
   PGPU_PATH_DENSE = 1,    /* sumset bytemap + per-interval private accumulators    */
   PGPU_PATH_SORT = 2,     /* expand / LSD radix sort / run-length reduce            */
-  PGPU_PATH_BUCKET = 3    /* pairs written once into key-range buckets of <= 2048,
+  PGPU_PATH_BUCKET = 3,   /* pairs written once into key-range buckets of <= 512,
                              each grouped and reduced by one CTA in shared memory
                              (a batch that does not suit it takes PATH_SORT)       */
+  PGPU_PATH_SMALL = 4     /* products of at most 8192 pairs in one CTA (sorted in
+                             shared memory, folded in the reference's row order);
+                             AUTO takes it for such products                        */
 } pgpu_path;
 
 /* Packed-exponent layout (reference Layout, core.py:65-121).  Fields are listed

@@ -15,7 +15,7 @@ NPHASE = 8
 
 PGPU_OK, PGPU_EINVAL, PGPU_EEXPONENT, PGPU_ECOEFF, PGPU_ECUDA, PGPU_ENOMEM, PGPU_EUNSUPPORTED = range(7)
 F64, I64, I128 = 0, 1, 2
-PATH_AUTO, PATH_DENSE, PATH_SORT, PATH_BUCKET = 0, 1, 2, 3
+PATH_AUTO, PATH_DENSE, PATH_SORT, PATH_BUCKET, PATH_SMALL = 0, 1, 2, 3, 4
 
 LIB_PATH = Path(__file__).resolve().parent / "lib" / "libpolymul_b200.so"
 # PGPU_LIB: load a different build of the same library (kernel-variant experiments)

@@ -32,6 +32,7 @@
 #include "format.cuh"
 #include "prep.cuh"
 #include "scan.cuh"
+#include "small_path.cuh"
 #include "sort_path.cuh"
 
 using namespace pgpu;
@@ -81,6 +82,7 @@ struct DeviceState {
   size_t mem_free0 = 0, mem_total = 0;  // device memory at first use (cudaMemGetInfo is
                                         // slow and occasionally blocks for milliseconds)
   std::mutex mu;       // one product per device at a time uses the workspace
+  uint8_t* stage = nullptr;  // pinned staging for small host operands (copy_in_small)
 };
 std::mutex g_mu;
 DeviceState g_dev[64];
@@ -1010,6 +1012,15 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   // packed [lo, hi) -> compact [KL, KH)
   pb.KL = 0;
   pb.KH = ~0ull;
+  const uint64_t npairs = (uint64_t)pb.na * pb.nb;
+  if (o.lo == 0 && o.hi == ~0ull && npairs <= (uint64_t)kSmallPairs &&
+      P.kbits + std::max(1, bitlen64(npairs - 1)) <= 63 && !getenv("PGPU_NO_SMALL") &&
+      (o.path == PGPU_PATH_AUTO || o.path == PGPU_PATH_SMALL)) {
+    // the one-CTA path needs neither thresholds nor key ends: no second round trip
+    pb.kmin = 0;
+    pb.kmax = ~0ull;
+    return PGPU_OK;
+  }
   unsigned long long* dthr;
   TRY(ctx.ar->alloc(&dthr, 2));
   unsigned long long init[2] = {~0ull, ~0ull};
@@ -1048,6 +1059,105 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   return PGPU_OK;
 }
 
+// Small products (<= kSmallPairs pairs): one CTA, one launch, one round trip.
+// Returns PGPU_OK with *done = false when the product does not qualify.
+template <typename KT, int NL, int CK>
+void launch_small(Ctx& ctx, const SmallArgs& A) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_small_product<KT, NL, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)kSmallSmem);
+    attr = true;
+  }
+  k_small_product<KT, NL, CK><<<1, kSmallThreads, kSmallSmem, ctx.st>>>(A);
+}
+
+template <typename KT>
+void launch_small_kind(Ctx& ctx, const Problem& pb, const SmallArgs& A) {
+  const int nl = pb.nl ? pb.nl : 1;
+  if (pb.ck == PGPU_F64) launch_small<KT, 1, 0>(ctx, A);
+  else if (pb.ck == PGPU_I64) {
+    if (nl == 1) launch_small<KT, 1, 1>(ctx, A);
+    else if (nl == 2) launch_small<KT, 2, 1>(ctx, A);
+    else launch_small<KT, 3, 1>(ctx, A);
+  } else {
+    if (nl == 1) launch_small<KT, 1, 2>(ctx, A);
+    else if (nl == 2) launch_small<KT, 2, 2>(ctx, A);
+    else launch_small<KT, 3, 2>(ctx, A);
+  }
+}
+
+int small_run(Ctx& ctx, const Problem& pb, const pgpu_options& o, pgpu_result* out, bool* done) {
+  *done = false;
+  const uint64_t pairs = (uint64_t)pb.na * pb.nb;
+  if (pairs == 0 || pairs > (uint64_t)kSmallPairs) return PGPU_OK;
+  const int pbits = std::max(1, bitlen64(pairs - 1));
+  if (pb.P.kbits + pbits > 63) return PGPU_OK;
+  const int nl = pb.nl ? pb.nl : 1;
+  Arena& ar = *ctx.ar;
+  uint64_t *oexp, *ocoef;
+  unsigned long long* cnt;
+  if (o.outputs_on_device) {
+    TRY(ar.alloc_out(&oexp, pairs));
+    TRY(ar.alloc_out(&ocoef, pairs * nl));
+  } else {
+    TRY(ar.alloc(&oexp, pairs));
+    TRY(ar.alloc(&ocoef, pairs * nl));
+  }
+  TRY(ar.alloc(&cnt, 2));
+  SmallArgs A;
+  A.ak = pb.ak;
+  A.bk = pb.bk;
+  A.ac = pb.acoef;
+  A.bc = pb.bcoef;
+  A.na = pb.na;
+  A.nb = pb.nb;
+  A.KL = pb.KL;
+  A.KH = pb.KH;
+  A.pbits = pbits;
+  A.P = pb.P;
+  A.oexp = oexp;
+  A.ocoef = ocoef;
+  A.count = cnt;
+  if (pb.k32) launch_small_kind<uint32_t>(ctx, pb, A);
+  else launch_small_kind<uint64_t>(ctx, pb, A);
+  LAUNCHED(1);
+  CUDA_TRY(cudaGetLastError());
+  ctx.tm.mark(1, "small");
+  out->acc_limbs = nl;
+  out->path_used = PGPU_PATH_SMALL;
+  unsigned long long n = 0, formed = 0;
+  if (o.outputs_on_device) {
+    unsigned long long hc[2];
+    CUDA_TRY(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaStreamSynchronize(ctx.st));
+    n = hc[0];
+    formed = hc[1];
+    ar.release(oexp);
+    ar.release(ocoef);
+    out->exps = oexp;
+    out->coeffs = ocoef;
+  } else {
+    // capacity-sized copies ride along with the count: one round trip
+    out->exps = (uint64_t*)g_pinned.get(pairs * 8 + 64);  // + the two counters
+    out->coeffs = g_pinned.get(pairs * 8 * nl);
+    out->_owner = (void*)kPinnedTag;
+    if (!out->exps || !out->coeffs) return fail(PGPU_ENOMEM, "pinned host allocation failed");
+    unsigned long long* hcnt = reinterpret_cast<unsigned long long*>(out->exps + pairs);
+    CUDA_TRY(cudaMemcpyAsync(out->exps, oexp, pairs * 8, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaMemcpyAsync(out->coeffs, ocoef, pairs * 8 * nl, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaMemcpyAsync(hcnt, cnt, 16, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaStreamSynchronize(ctx.st));
+    n = hcnt[0];
+    formed = hcnt[1];
+  }
+  out->n = (int64_t)n;
+  out->pairs = (int64_t)formed;
+  ctx.tm.mark(5, "output");
+  *done = true;
+  return PGPU_OK;
+}
+
 int copy_in(Ctx& ctx, const pgpu_poly* p, size_t csz, const pgpu_options& o, const uint64_t** exps,
             const void** coef) {
   if (o.inputs_on_device) {
@@ -1063,6 +1173,33 @@ int copy_in(Ctx& ctx, const pgpu_poly* p, size_t csz, const pgpu_options& o, con
   CUDA_TRY(cudaMemcpyAsync(c, p->coeffs, p->n * csz, cudaMemcpyHostToDevice, ctx.st));
   *exps = e;
   *coef = c;
+  return PGPU_OK;
+}
+
+constexpr size_t kSmallStage = 1 << 20;
+
+// Small host operands: packed into the device's pinned staging buffer and sent
+// in one copy.  The caller holds the device lock and every product ends with a
+// stream synchronisation, so the buffer is free again when the next call starts.
+int copy_in_small(Ctx& ctx, DeviceState& dev, const pgpu_poly* a, const pgpu_poly* b, size_t csz,
+                  Problem* pb) {
+  if (!dev.stage) CUDA_TRY(cudaMallocHost((void**)&dev.stage, kSmallStage));
+  uint8_t* g_stage = dev.stage;
+  const size_t ea = (size_t)a->n * 8, ca = (size_t)a->n * csz, eb = (size_t)b->n * 8, cb = (size_t)b->n * csz;
+  // 16-byte aligned sections: exps a | coef a | exps b | coef b
+  auto up = [](size_t x) { return (x + 15) & ~size_t(15); };
+  const size_t oa = 0, oca = up(ea), ob = oca + up(ca), ocb = ob + up(eb), tot = ocb + up(cb);
+  memcpy(g_stage + oa, a->exps, ea);
+  memcpy(g_stage + oca, a->coeffs, ca);
+  memcpy(g_stage + ob, b->exps, eb);
+  memcpy(g_stage + ocb, b->coeffs, cb);
+  uint8_t* d;
+  TRY(ctx.ar->alloc(&d, tot));
+  CUDA_TRY(cudaMemcpyAsync(d, g_stage, tot, cudaMemcpyHostToDevice, ctx.st));
+  pb->aexp = reinterpret_cast<const uint64_t*>(d + oa);
+  pb->acoef = d + oca;
+  pb->bexp = reinterpret_cast<const uint64_t*>(d + ob);
+  pb->bcoef = d + ocb;
   return PGPU_OK;
 }
 
@@ -1101,12 +1238,31 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   pb.na = (uint32_t)a->n;
   pb.nb = (uint32_t)b->n;
   size_t csz = o.coef_kind == PGPU_I128 ? 16 : 8;
-  TRY(copy_in(ctx, a, csz, o, &pb.aexp, &pb.acoef));
-  TRY(copy_in(ctx, b, csz, o, &pb.bexp, &pb.bcoef));
+  const size_t in_bytes = (size_t)(a->n + b->n) * (8 + csz);
+  if (!o.inputs_on_device && in_bytes <= kSmallStage) {
+    // small operands: one pinned staging buffer, one host-to-device copy
+    TRY(copy_in_small(ctx, dstate, a, b, csz, &pb));
+  } else {
+    TRY(copy_in(ctx, a, csz, o, &pb.aexp, &pb.acoef));
+    TRY(copy_in(ctx, b, csz, o, &pb.bexp, &pb.bcoef));
+  }
   TRY(build_problem(ctx, lay, opt, pb, o));
   out->key_bits = pb.P.kbits;
   out->acc_limbs = pb.nl ? pb.nl : 1;
 
+  // small products: one CTA, one launch, one host round trip
+  if (pb.KL < pb.KH && (o.path == PGPU_PATH_AUTO || o.path == PGPU_PATH_SMALL) &&
+      !getenv("PGPU_NO_SMALL")) {
+    ctx.tm.mark(0, "prep");
+    bool done = false;
+    TRY(small_run(ctx, pb, o, out, &done));
+    if (done) {
+      ctx.tm.finish(out);
+      CUDA_TRY(cudaGetLastError());
+      out->kernel_launches = ctx.launches;
+      return PGPU_OK;
+    }
+  }
   std::vector<Slice> slices;
   if (pb.KL < pb.KH) {
     // total pairs in range
@@ -1128,6 +1284,7 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
     int path = o.path;
     if (o.float_ordered && o.coef_kind == PGPU_F64) path = PGPU_PATH_SORT;
     int used = PGPU_PATH_SORT;
+    if (path == PGPU_PATH_SMALL) path = PGPU_PATH_AUTO;  // product too large for one CTA
     if (path != PGPU_PATH_SORT && path != PGPU_PATH_BUCKET) {
       int r = dense_try(ctx, pb, total, slices, path == PGPU_PATH_DENSE, &used);
       if (r != PGPU_OK) return r;

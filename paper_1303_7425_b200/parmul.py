@@ -28,8 +28,9 @@ from .core import (SENTINEL, CoefficientOverflowError, ExponentOverflowError, ch
                    check_product_fits)
 
 MERGERS = ("heap", "tree")
-PATHS = {"auto": N.PATH_AUTO, "dense": N.PATH_DENSE, "sort": N.PATH_SORT, "bucket": N.PATH_BUCKET}
-PATH_NAMES = {1: "dense", 2: "sort", 3: "bucket"}
+PATHS = {"auto": N.PATH_AUTO, "dense": N.PATH_DENSE, "sort": N.PATH_SORT, "bucket": N.PATH_BUCKET,
+         "small": N.PATH_SMALL}
+PATH_NAMES = {1: "dense", 2: "sort", 3: "bucket", 4: "small"}
 DEFAULT_GRID_DENSITY = 64
 _M64 = (1 << 64) - 1
 
@@ -41,7 +42,7 @@ class MulConfig:
     l, c, merger  -- as in the reference; `merger` names the CPU merge the
                      reference would use and is validated the same way; both
                      produce identical output (merge.py:1-16), as does the GPU.
-    path          -- "auto" | "dense" | "sort" | "bucket" (device algorithm)
+    path          -- "auto" | "dense" | "sort" | "bucket" | "small" (device algorithm)
     float_ordered -- fold float coefficients in the reference's row order so
                      doubles are bit-identical to the CPU (sort path)
     device        -- CUDA ordinal

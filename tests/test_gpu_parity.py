@@ -31,7 +31,7 @@ def _check(got, want, ordered_float=True, a=None, b=None):
         assert got.exps == [int(e) for e in want["exps"]]
 
 
-@pytest.mark.parametrize("path", ["auto", "sort", "bucket"])
+@pytest.mark.parametrize("path", ["auto", "sort", "bucket", "small"])
 @pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
 def test_golden_cases(case, path):
     name, a, b, split, want = case
@@ -337,7 +337,7 @@ def test_bucket_path_random_sparse_vs_oracle(ctype, rng):
             assert np.allclose(got.coef, np.asarray(want.coeffs), rtol=1e-12, atol=1e-9)
 
 
-@pytest.mark.parametrize("path", ["auto", "dense", "bucket", "sort"])
+@pytest.mark.parametrize("path", ["auto", "dense", "bucket", "sort", "small"])
 def test_degenerate_shapes_and_field_limits(path):
     """1xN, Nx1 and 1x1 products, exponents exactly at the field caps (the
     reference's overflow test is componentwise max <= cap, core.py:365-385),
@@ -365,3 +365,25 @@ def test_degenerate_shapes_and_field_limits(path):
         assert got.exps == want.exps and got.coeffs == want.coeffs
     with pytest.raises(ExponentOverflowError):
         mul(hi, Polynomial(lay, [(1, (m + 1, 0, 0))], int), MulConfig(path=path))
+
+
+def test_small_path_is_taken_and_exact(rng):
+    """Products of at most 8192 pairs run in one CTA (path_used 'small') and
+    equal the oracle, floats bit for bit in the reference's row order."""
+    from oracle import oracle as O
+    from paper_1303_7425_b200.core import Polynomial as P
+    lay = default_layout(("x", "y", "z"))
+    for ctype in (int, float):
+        for na, nb in [(1, 1), (3, 50), (90, 91), (64, 128)]:
+            terms = lambda n: [((rng.randint(-99, 99) or 1) if ctype is int else rng.uniform(-2, 2),
+                                tuple(rng.randint(0, 6) for _ in range(3))) for _ in range(n)]
+            a, b = P(lay, terms(na), ctype), P(lay, terms(nb), ctype)
+            raw = native_mul(Operand.from_poly(a), Operand.from_poly(b), lay)
+            assert raw.path == "small" and raw.pairs == a.n * b.n
+            want = O.mul(a, b)
+            assert raw.exps.tolist() == want.exps
+            if ctype is float:
+                assert raw.coef.tolist() == want.coeffs  # reference order: bit-identical
+            else:
+                from paper_1303_7425_b200.parmul import limbs_to_ints
+                assert limbs_to_ints(raw.coef, raw.nl) == want.coeffs
