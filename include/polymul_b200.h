@@ -78,7 +78,7 @@ typedef enum pgpu_path {
   PGPU_PATH_BUCKET = 3,   /* pairs written once into key-range buckets of <= 512,
                              each grouped and reduced by one CTA in shared memory
                              (a batch that does not suit it takes PATH_SORT)       */
-  PGPU_PATH_SMALL = 4     /* products of at most 8192 pairs in one CTA (sorted in
+  PGPU_PATH_SMALL = 4     /* products of at most 16384 pairs in one CTA (sorted in
                              shared memory, folded in the reference's row order);
                              AUTO takes it for such products                        */
 } pgpu_path;

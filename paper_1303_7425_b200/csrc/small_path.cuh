@@ -14,7 +14,10 @@
 
 namespace pgpu {
 
-constexpr int kSmallPairs = 8192;  // 64 KB of sort words
+#ifndef PGPU_SMALL_PAIRS
+#define PGPU_SMALL_PAIRS 16384
+#endif
+constexpr int kSmallPairs = PGPU_SMALL_PAIRS;  // 8 B sort word + 2 B head each, in shared memory
 constexpr int kSmallThreads = 1024;
 constexpr size_t kSmallSmem = kSmallPairs * 8 + (kSmallPairs + 8) * 2;
 

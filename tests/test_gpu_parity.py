@@ -368,7 +368,7 @@ def test_degenerate_shapes_and_field_limits(path):
 
 
 def test_small_path_is_taken_and_exact(rng):
-    """Products of at most 8192 pairs run in one CTA (path_used 'small') and
+    """Products of at most 16384 pairs run in one CTA (path_used 'small') and
     equal the oracle, floats bit for bit in the reference's row order."""
     from oracle import oracle as O
     from paper_1303_7425_b200.core import Polynomial as P
