@@ -387,3 +387,30 @@ def test_small_path_is_taken_and_exact(rng):
             else:
                 from paper_1303_7425_b200.parmul import limbs_to_ints
                 assert limbs_to_ints(raw.coef, raw.nl) == want.coeffs
+
+
+def test_concurrent_callers_share_the_device():
+    """Several host threads multiplying on the same GPU at once (ctypes drops
+    the GIL; the library serialises products per device): every result exact."""
+    import threading
+    prods = [benchpolys.fateman(6), benchpolys.monagan_pearce(4), benchpolys.fateman(3)]
+    want = [mul(f, g) for f, g in prods]
+    errors = []
+
+    def worker(k):
+        try:
+            for r in range(12):
+                f, g = prods[(k + r) % len(prods)]
+                p = mul(f, g, MulConfig(path=("auto", "sort", "bucket")[(k + r) % 3]))
+                w = want[(k + r) % len(prods)]
+                if p.exps != w.exps or p.coeffs != w.coeffs:
+                    errors.append((k, r))
+        except Exception as exc:  # pragma: no cover - reported below
+            errors.append(repr(exc))
+
+    threads = [threading.Thread(target=worker, args=(k,)) for k in range(4)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join()
+    assert not errors, errors
