@@ -60,6 +60,9 @@ constexpr int kRsWarps = kRsThreads / 32;
 #ifndef PGPU_RS_IPT
 #define PGPU_RS_IPT 12
 #endif
+#ifndef PGPU_RS_LOOKBACK
+#define PGPU_RS_LOOKBACK 4
+#endif
 constexpr int kRsIpt = PGPU_RS_IPT;                // items per thread per tile
 constexpr int kRsTile = kRsThreads * kRsIpt;       // 4096
 constexpr int kRsDigits = 256;
@@ -190,6 +193,27 @@ k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* 
       *st = kFlagAgg | sum;
       unsigned long long excl = 0;
       int64_t k = (int64_t)t - 1;
+#if PGPU_RS_LOOKBACK > 1
+      // kLook predecessors per round trip: the chain of aggregate-only tiles
+      // is walked kLook tiles at a time instead of one
+      constexpr int kLook = PGPU_RS_LOOKBACK;
+      for (bool done = false; !done;) {
+        unsigned long long v[kLook];
+#pragma unroll
+        for (int u = 0; u < kLook; ++u)
+          v[u] = k - u >= 0 ? *(volatile unsigned long long*)(status + (uint64_t)(k - u) * kRsDigits + d)
+                            : (2ull << 62);  // before tile 0: an inclusive zero
+#pragma unroll
+        for (int u = 0; u < kLook; ++u) {
+          if (done) break;
+          const unsigned long long flag = v[u] & ~kValMask;
+          if (flag == 0) break;  // not published yet: re-poll from here
+          excl += v[u] & kValMask;
+          --k;
+          if (flag == kFlagPre) done = true;
+        }
+      }
+#else
       for (;;) {
         const unsigned long long v = *(volatile unsigned long long*)(status + (uint64_t)k * kRsDigits + d);
         const unsigned long long flag = v & ~kValMask;
@@ -198,6 +222,7 @@ k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* 
         if (flag == kFlagPre) break;
         --k;
       }
+#endif
       *st = kFlagPre | (excl + sum);
       gpre[d] = excl;
     }
