@@ -366,482 +366,11 @@ int count_at(Ctx& ctx, const Problem& pb, const std::vector<uint64_t>& bounds,
   return PGPU_OK;
 }
 
-// ---------------------------------------------------------------------------
-// Sort path over one compact key range [KL, KH) holding `pairs` pairs.
-// ---------------------------------------------------------------------------
-template <typename KT>
-int radix_sort(Ctx& ctx, KT** keys, uint64_t** vals, KT* kalt, uint64_t* valt, uint64_t n,
-               int bits) {
-  if (n <= 1 || bits <= 0) return PGPU_OK;
-  const int npass = (bits + 7) / 8;
-  if (npass > kRsMaxPasses) return fail(PGPU_EUNSUPPORTED, "sort key wider than 64 bits");
-  const uint64_t ntiles = (n + kRsTile - 1) / kRsTile;
-  unsigned int* ghist;
-  unsigned long long* status;
-  unsigned int* ctr;
-  TRY(ctx.ar->alloc(&ghist, (size_t)kRsMaxPasses * kRsDigits));
-  TRY(ctx.ar->alloc(&status, (size_t)ntiles * kRsDigits));
-  TRY(ctx.ar->alloc(&ctr, npass));
-  CUDA_TRY(cudaMemsetAsync(ghist, 0, sizeof(unsigned int) * kRsMaxPasses * kRsDigits, ctx.st));
-  CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned int) * npass, ctx.st));
-  k_rs_hist_all<KT><<<grid_for((int64_t)((n + kRsThreads - 1) / kRsThreads), 1, ctx.sms * 8),
-                      kRsThreads, 0, ctx.st>>>(*keys, n, npass, ghist);
-  k_rs_hist_scan<<<1, kRsDigits, 0, ctx.st>>>(ghist, npass);
-  LAUNCHED(2);
-  const size_t smem = (sizeof(KT) + 8) * (size_t)kRsTile;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_rs_onesweep<KT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    attr_set = true;
-  }
-  KT* kin = *keys;
-  uint64_t* vin = *vals;
-  KT* kout = kalt;
-  uint64_t* vout = valt;
-  for (int p = 0; p < npass; ++p) {
-    CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(unsigned long long) * ntiles * kRsDigits, ctx.st));
-    k_rs_onesweep<KT><<<(unsigned)ntiles, kRsThreads, smem, ctx.st>>>(
-        kin, vin, kout, vout, n, 8 * p, ghist + p * kRsDigits, status, ctr + p);
-    LAUNCHED(1);
-    std::swap(kin, kout);
-    std::swap(vin, vout);
-  }
-  *keys = kin;
-  *vals = vin;
-  return PGPU_OK;
-}
+// Sort path driver (kernels in sort_path.cuh)
+#include "sort_driver.inc"
 
-template <typename KT, typename RT>
-int sort_range_rt(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
-                  uint64_t pairs, int bits, Slice* out);
-
-// local key width: keys are stored relative to KL, in 32 bits when they fit
-template <typename KT>
-int sort_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
-                    uint64_t pairs, Slice* out) {
-  out->n = 0;
-  if (pairs == 0) return PGPU_OK;
-  uint64_t kmax_local = std::min<uint64_t>(KH == ~0ull ? pb.kmax : KH - 1, pb.kmax) - KL;
-  int bits = bitlen64(kmax_local);
-  if (bits <= 32) return sort_range_rt<KT, uint32_t>(ctx, outer, pb, KL, KH, pairs, bits, out);
-  return sort_range_rt<KT, uint64_t>(ctx, outer, pb, KL, KH, pairs, bits, out);
-}
-
-// One batch: its scratch lives in a batch-scoped arena (returned to the pool
-// before the next batch); only the compacted output is owned by the caller's arena.
-template <typename KT>
-int sort_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t pairs, Slice* out) {
-  Arena* outer = ctx.ar;
-  int r;
-  if (ctx.batch_blk) {  // large products: the batch block allocated once per product
-    Arena batch(ctx.st, ctx.batch_blk, ctx.batch_cap);
-    ctx.ar = &batch;
-    r = sort_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out);
-    ctx.ar = outer;
-    return r;
-  }
-  // nested: small batches bump-allocate above the caller's workspace usage
-  Arena batch(ctx.st, pairs * 48 < (64ull << 20) ? outer->dev : nullptr, outer->used);
-  ctx.ar = &batch;
-  r = sort_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out);
-  ctx.ar = outer;
-  return r;
-}
-
-template <typename KT, typename RT>
-int sort_range_rt(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
-                  uint64_t pairs, int bits, Slice* out) {
-  uint32_t *rlo, *rhi;
-  uint64_t* off;
-  uint64_t chk;
-  TRY(range_rows<KT>(ctx, pb, KL, KH, &rlo, &rhi, &off, &chk));
-  if (chk != pairs) return fail(PGPU_ECUDA, "pair count mismatch %llu vs %llu",
-                                (unsigned long long)chk, (unsigned long long)pairs);
-  RT *keys, *kalt;
-  uint64_t *vals, *valt;
-  TRY(ctx.ar->alloc(&keys, pairs));
-  TRY(ctx.ar->alloc(&vals, pairs));
-  TRY(ctx.ar->alloc(&kalt, pairs));
-  TRY(ctx.ar->alloc(&valt, pairs));
-  k_gen<KT, RT><<<grid_for((int64_t)pb.na * 32, 256, ctx.sms * 16), 256, 0, ctx.st>>>(
-      (const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, off, pb.na, KL, keys, vals);
-  LAUNCHED(1);
-  ctx.tm.mark(1, "gen");
-  TRY(radix_sort<RT>(ctx, &keys, &vals, kalt, valt, pairs, bits));
-  ctx.tm.mark(2, "sort");
-  // heads -> segment starts (reuse the spare buffer as starts)
-  uint32_t* starts;
-  TRY(ctx.ar->alloc(&starts, pairs + 1));
-  uint32_t* part;
-  TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
-  int g;
-  LAUNCHED(device_scan<uint32_t>(pairs, HeadGen<RT>{keys}, HeadOut{starts}, part, &g, ctx.st));
-  uint32_t nseg;
-  CUDA_TRY(cudaMemcpyAsync(&nseg, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  uint32_t pe = (uint32_t)pairs;
-  CUDA_TRY(cudaMemcpyAsync(starts + nseg, &pe, 4, cudaMemcpyHostToDevice, ctx.st));
-  int nl = pb.nl ? pb.nl : 1;
-  uint64_t *sexp, *scoef;
-  uint32_t* snz;
-  TRY(ctx.ar->alloc(&sexp, nseg));
-  TRY(ctx.ar->alloc(&scoef, (size_t)nseg * nl));
-  TRY(ctx.ar->alloc(&snz, nseg));
-  int gr = grid_for(nseg, 256, 1 << 30);
-  if (pb.ck == PGPU_F64) {
-    k_seg_reduce_f64<RT><<<gr, 256, 0, ctx.st>>>(keys, vals, starts, nseg, (const double*)pb.acoef,
-                                                (const double*)pb.bcoef, KL, pb.P, sexp,
-                                                (double*)scoef, snz);
-  } else {
-    // lanes per segment from the mean segment length (about 16-24 pairs per lane)
-    const uint64_t mean = pairs / std::max<uint32_t>(nseg, 1);
-    int G = 1;
-    while (G < 32 && (uint64_t)G * 24 < mean) G <<= 1;  // MP n=25 (mean 65): G = 4, measured best
-    if (const char* e = getenv("PGPU_SEG_LANES")) G = atoi(e);
-    const int grg = grid_for((int64_t)nseg * G, 256, 1 << 30);
-#define SEGRED_G(NL_, CK_, G_)                                                                    \
-  k_seg_reduce_int<RT, NL_, CK_, G_><<<grg, 256, 0, ctx.st>>>(keys, vals, starts, nseg, pb.acoef, \
-                                                              pb.bcoef, KL, pb.P, sexp, scoef, snz)
-#define SEGRED(NL_, CK_)                         \
-  do {                                           \
-    switch (G) {                                 \
-      case 1: SEGRED_G(NL_, CK_, 1); break;      \
-      case 2: SEGRED_G(NL_, CK_, 2); break;      \
-      case 4: SEGRED_G(NL_, CK_, 4); break;      \
-      case 8: SEGRED_G(NL_, CK_, 8); break;      \
-      case 16: SEGRED_G(NL_, CK_, 16); break;    \
-      default: SEGRED_G(NL_, CK_, 32); break;    \
-    }                                            \
-  } while (0)
-    if (pb.ck == PGPU_I64) {
-      if (nl == 1) SEGRED(1, 1); else if (nl == 2) SEGRED(2, 1); else SEGRED(3, 1);
-    } else {
-      if (nl == 1) SEGRED(1, 2); else if (nl == 2) SEGRED(2, 2); else SEGRED(3, 2);
-    }
-#undef SEGRED
-#undef SEGRED_G
-  }
-  LAUNCHED(1);
-  ctx.tm.mark(3, "reduce");
-  // compaction of zero sums
-  uint64_t *cexp, *ccoef;
-  TRY(outer->alloc_out(&cexp, nseg));
-  TRY(outer->alloc_out(&ccoef, (size_t)nseg * nl));
-  LAUNCHED(device_scan<uint32_t>(nseg, FlagGen{snz}, CompactOut{sexp, scoef, nl, cexp, ccoef}, part,
-                                 &g, ctx.st));
-  uint32_t nnz;
-  CUDA_TRY(cudaMemcpyAsync(&nnz, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  ctx.tm.mark(4, "compact");
-  out->exps = cexp;
-  out->coef = ccoef;
-  out->n = nnz;
-  return PGPU_OK;
-}
-
-// Split [KL, KH) into ranges of at most `cap` pairs, in ascending key order.
-// max_span (0 = none): also keep every range's key span within max_span, so
-// that its records carry 32-bit local keys (4 radix passes of 12-byte records
-// instead of 5 of 16 bytes for 33..40-bit compact keys).
-template <typename KT>
-int plan_batches(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t total,
-                 uint64_t cap, std::vector<std::pair<uint64_t, uint64_t>>& ranges,
-                 std::vector<uint64_t>& counts, uint64_t max_span = 0) {
-  ranges.clear();
-  counts.clear();
-  const uint64_t keyend = pb.kmax + 1;  // effective end of the open top range
-  auto eff = [&](uint64_t b) { return b == ~0ull ? keyend : b; };
-  if (total <= cap && (max_span == 0 || eff(KH) - KL <= max_span)) {
-    ranges.push_back({KL, KH});
-    counts.push_back(total);
-    return PGPU_OK;
-  }
-  // candidate bounds: sums on a 64x64 grid of the pair matrix
-  std::vector<uint64_t> ak(pb.na), bk(pb.nb);
-  if (pb.k32) {
-    std::vector<uint32_t> a32(pb.na), b32(pb.nb);
-    CUDA_TRY(cudaMemcpyAsync(a32.data(), pb.ak, 4ull * pb.na, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(b32.data(), pb.bk, 4ull * pb.nb, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaStreamSynchronize(ctx.st));
-    for (uint32_t i = 0; i < pb.na; ++i) ak[i] = a32[i];
-    for (uint32_t j = 0; j < pb.nb; ++j) bk[j] = b32[j];
-  } else {
-    CUDA_TRY(cudaMemcpyAsync(ak.data(), pb.ak, 8ull * pb.na, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(bk.data(), pb.bk, 8ull * pb.nb, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  }
-  std::vector<uint64_t> cand;
-  const int L = 64;
-  for (int r = 0; r <= L; ++r)
-    for (int c = 0; c <= L; ++c) {
-      uint64_t i = std::min<uint64_t>((uint64_t)r * pb.na / L, pb.na - 1);
-      uint64_t j = std::min<uint64_t>((uint64_t)c * pb.nb / L, pb.nb - 1);
-      uint64_t k = ak[i] + bk[j];
-      if (k > KL && k < KH) cand.push_back(k);
-    }
-  std::sort(cand.begin(), cand.end());
-  cand.erase(std::unique(cand.begin(), cand.end()), cand.end());
-  std::vector<uint64_t> cum;
-  TRY(count_at<KT>(ctx, pb, cand, cum));
-  uint64_t below_KL;
-  {
-    std::vector<uint64_t> c0, b0{KL};
-    TRY(count_at<KT>(ctx, pb, b0, c0));
-    below_KL = c0[0];
-  }
-  // bounds list with cumulative counts (relative to KL)
-  std::vector<uint64_t> bnd{KL}, cm{0};
-  for (size_t k = 0; k < cand.size(); ++k) {
-    bnd.push_back(cand[k]);
-    cm.push_back(cum[k] - below_KL);
-  }
-  bnd.push_back(KH);
-  cm.push_back(total);
-  // refine oversize gaps by bisection in key space
-  for (size_t k = 0; k + 1 < bnd.size();) {
-    uint64_t c = cm[k + 1] - cm[k];
-    uint64_t hiK = bnd[k + 1];
-    if (hiK == ~0ull) {
-      // bound the open top by the largest possible key + 1
-      hiK = ak[pb.na - 1] + bk[pb.nb - 1] + 1;
-    }
-    if ((c > cap || (max_span && hiK - bnd[k] > max_span)) && hiK - bnd[k] > 1) {
-      uint64_t mid = bnd[k] + (hiK - bnd[k]) / 2;
-      std::vector<uint64_t> cc, bb{mid};
-      TRY(count_at<KT>(ctx, pb, bb, cc));
-      bnd.insert(bnd.begin() + k + 1, mid);
-      cm.insert(cm.begin() + k + 1, cc[0] - below_KL);
-      continue;
-    }
-    if (c > cap)
-      return fail(PGPU_EUNSUPPORTED, "a single key holds %llu pairs, more than the batch "
-                                     "capacity %llu", (unsigned long long)c,
-                  (unsigned long long)cap);
-    ++k;
-  }
-  // greedy packing
-  size_t k = 0;
-  while (k + 1 < bnd.size()) {
-    size_t e = k + 1;
-    while (e + 1 < bnd.size() && cm[e + 1] - cm[k] <= cap &&
-           (max_span == 0 || eff(bnd[e + 1]) - bnd[k] <= max_span))
-      ++e;
-    ranges.push_back({bnd[k], bnd[e]});
-    counts.push_back(cm[e] - cm[k]);
-    k = e;
-  }
-  return PGPU_OK;
-}
-
-
-// ---------------------------------------------------------------------------
-// Bucket path over one key range (bucket_path.cuh).  *done = false when the
-// range does not suit it (a fine bin above the bucket bound, staging
-// overflow, key span too wide): the caller then runs the sort path.
-// ---------------------------------------------------------------------------
-template <typename KT, int NL, int CK>
-void launch_bucket_reduce(Ctx& ctx, uint32_t K, const BucketArgs& A) {
-  const size_t smem = sizeof(BucketSmem<KT, NL>);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_bucket_reduce<KT, NL, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr = true;
-  }
-  k_bucket_reduce<KT, NL, CK><<<K, kBucketThreads, smem, ctx.st>>>(A);
-}
-
-constexpr uint64_t kBucketMaxPairs = 1ull << 28;
-
-template <typename KT>
-int bucket_range_impl(Ctx& ctx, Arena* outer, const Problem& pb, uint64_t KL, uint64_t KH,
-                      uint64_t pairs, Slice* out, bool* done) {
-  *done = false;
-  out->n = 0;
-  if (pairs == 0) {
-    *done = true;
-    return PGPU_OK;
-  }
-  // The record scatter is random at pair granularity: it pays while the
-  // batch's records stay mostly L2/row-buffer friendly (MP n=12: 38M pairs,
-  // 2.4 ms vs 2.9 ms sorted).  At MP n=25 scale (2e9 pairs per batch) the
-  // partial-sector writes run at ~0.3 TB/s and the radix sort wins.
-  if (pairs > kBucketMaxPairs) return PGPU_OK;
-  // largest local key: the batch's upper bound, or the largest pair sum
-  const uint64_t span = std::min<uint64_t>(KH == ~0ull ? pb.kmax : KH - 1, pb.kmax) - KL;
-  if (span >= (1ull << 52)) return PGPU_OK;
-  // all-ones marks an empty hash slot: a record key may not take that value
-  if (sizeof(KT) == 4 && span >= 0xffffffffull) return PGPU_OK;
-  uint32_t *rlo, *rhi;
-  uint64_t* off;
-  uint64_t chk;
-  TRY(range_rows<KT>(ctx, pb, KL, KH, &rlo, &rhi, &off, &chk));
-  if (chk != pairs) return fail(PGPU_ECUDA, "pair count mismatch %llu vs %llu",
-                                (unsigned long long)chk, (unsigned long long)pairs);
-  // level 1: coarse bins (at most 2^22, ~16 pairs each on average)
-  const uint64_t target = std::max<uint64_t>(1, std::min<uint64_t>(pairs / 16, 1ull << 22));
-  const int s1 = std::max(0, bitlen64(span) - bitlen64(target - 1));
-  const uint32_t ncoarse = (uint32_t)((span >> s1) + 1);
-  uint32_t *hist1, *tab, *flags;  // flags[1]: the reduce kernel's fallback flag
-  TRY(ctx.ar->alloc(&hist1, ncoarse));
-  TRY(ctx.ar->alloc(&tab, ncoarse));
-  TRY(ctx.ar->alloc(&flags, 4));
-  CUDA_TRY(cudaMemsetAsync(hist1, 0, 4ull * ncoarse, ctx.st));
-  CUDA_TRY(cudaMemsetAsync(flags, 0, 16, ctx.st));
-  const int wgrid = grid_for((int64_t)pb.na * 32, 256, ctx.sms * 16);
-  k_bin_count<KT><<<wgrid, 256, 0, ctx.st>>>((const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, pb.na,
-                                             KL, BinMap{s1, nullptr}, hist1);
-  LAUNCHED(1);
-  uint32_t* part;
-  TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
-  int g;
-  // level 2: split coarse bins into ~kBinTarget-pair fine bins
-  RefineGen rg{hist1, s1};
-  LAUNCHED(device_scan<uint32_t>(ncoarse, rg, RefineOut{rg, tab}, part, &g, ctx.st));
-  uint32_t nbins;
-  CUDA_TRY(cudaMemcpyAsync(&nbins, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  const BinMap map{s1, tab};
-  uint32_t *hist, *binoff;
-  TRY(ctx.ar->alloc(&hist, nbins));
-  TRY(ctx.ar->alloc(&binoff, nbins));
-  CUDA_TRY(cudaMemsetAsync(hist, 0, 4ull * nbins, ctx.st));
-  k_bin_count<KT><<<wgrid, 256, 0, ctx.st>>>((const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, pb.na,
-                                             KL, map, hist);
-  LAUNCHED(1);
-  LAUNCHED(device_scan<uint32_t>(nbins, HistGen{hist}, BinOffOut{binoff}, part, &g, ctx.st));
-  // buckets (BStartGen): runs of small bins, big bins on their own
-  uint32_t* bstart;
-  TRY(ctx.ar->alloc(&bstart, (size_t)nbins + 1));
-  LAUNCHED(device_scan<uint32_t>(nbins, BStartGen{hist, binoff}, BStartOut{bstart}, part, &g, ctx.st));
-  uint32_t K;
-  CUDA_TRY(cudaMemcpyAsync(&K, part + g, 4, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  CUDA_TRY(cudaMemcpyAsync(bstart + K, &nbins, 4, cudaMemcpyHostToDevice, ctx.st));
-  if (getenv("PGPU_DEBUG"))
-    fprintf(stderr, "[pgpu] bucket range pairs=%llu span=%llu s1=%d coarse=%u fine=%u buckets=%u\n",
-            (unsigned long long)pairs, (unsigned long long)span, s1, ncoarse, nbins, K);
-  ctx.tm.mark(6, "bucket_bins");
-  // fill cursors start at the bin offsets (hist is reused)
-  CUDA_TRY(cudaMemcpyAsync(hist, binoff, 4ull * nbins, cudaMemcpyDeviceToDevice, ctx.st));
-  KT* rkey;
-  uint64_t* rid;
-  TRY(ctx.ar->alloc(&rkey, pairs));
-  TRY(ctx.ar->alloc(&rid, pairs));
-  k_bin_scatter<KT><<<wgrid, 256, 0, ctx.st>>>((const KT*)pb.ak, (const KT*)pb.bk, rlo, rhi, pb.na,
-                                               KL, map, hist, rkey, rid);
-  LAUNCHED(1);
-  ctx.tm.mark(6, "bucket_bins");
-  if (getenv("PGPU_DEBUG") && atoi(getenv("PGPU_DEBUG")) >= 2) {  // record invariants
-    std::vector<KT> hk(pairs), ha(pb.na), hb(pb.nb);
-    std::vector<uint64_t> hid(pairs);
-    std::vector<uint32_t> hoff(nbins);
-    CUDA_TRY(cudaMemcpyAsync(hk.data(), rkey, sizeof(KT) * pairs, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(hid.data(), rid, 8 * pairs, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(hoff.data(), binoff, 4ull * nbins, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(ha.data(), pb.ak, sizeof(KT) * pb.na, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(hb.data(), pb.bk, sizeof(KT) * pb.nb, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaStreamSynchronize(ctx.st));
-    int bad = 0;
-    uint32_t b = 0;
-    for (uint64_t q = 0; q < pairs && bad < 10; ++q) {
-      while (b + 1 < nbins && hoff[b + 1] <= q) ++b;
-      uint64_t i = hid[q] >> 32, j = hid[q] & 0xffffffffu;
-      uint64_t key = (uint64_t)ha[i] + hb[j] - KL;
-      if ((uint64_t)hk[q] != key) {  // (bins are not checked here)
-        fprintf(stderr, "[pgpu] record %llu: key %llu id (%llu,%llu) -> %llu, bin %u\n",
-                (unsigned long long)q, (unsigned long long)hk[q], (unsigned long long)i,
-                (unsigned long long)j, (unsigned long long)key, b);
-        ++bad;
-      }
-    }
-    fprintf(stderr, "[pgpu] record check done (%d bad)\n", bad);
-  }
-  const int nl = pb.nl ? pb.nl : 1;
-  // staging holds every distinct term in the worst case (sparse products with
-  // few collisions have almost as many terms as pairs); batches here are
-  // <= 2^28 pairs, so this is at most 2^28 * 32 B
-  const uint64_t scap = pairs;
-  uint64_t *sexp, *scoef, *bbase;
-  uint32_t* bnnz;
-  unsigned long long* sctr;
-  TRY(ctx.ar->alloc(&sexp, scap));
-  TRY(ctx.ar->alloc(&scoef, scap * nl));
-  TRY(ctx.ar->alloc(&bbase, K));
-  TRY(ctx.ar->alloc(&bnnz, K));
-  TRY(ctx.ar->alloc(&sctr, 1));
-  CUDA_TRY(cudaMemsetAsync(sctr, 0, 8, ctx.st));
-  BucketArgs A;
-  A.rkey = rkey;
-  A.rid = rid;
-  A.binoff = binoff;
-  A.bstart = bstart;
-  A.nbins = nbins;
-  A.pairs = (uint32_t)pairs;
-  A.s1 = s1;
-  A.tab = tab;
-  A.ac = pb.acoef;
-  A.bc = pb.bcoef;
-  A.KL = KL;
-  A.P = pb.P;
-  A.sexp = sexp;
-  A.scoef = scoef;
-  A.scap = scap;
-  A.sctr = sctr;
-  A.bbase = bbase;
-  A.bnnz = bnnz;
-  A.overflow = flags + 1;
-  if (pb.ck == PGPU_F64) {
-    launch_bucket_reduce<KT, 1, 0>(ctx, K, A);
-  } else if (pb.ck == PGPU_I64) {
-    if (nl == 1) launch_bucket_reduce<KT, 1, 1>(ctx, K, A);
-    else if (nl == 2) launch_bucket_reduce<KT, 2, 1>(ctx, K, A);
-    else launch_bucket_reduce<KT, 3, 1>(ctx, K, A);
-  } else {
-    if (nl == 1) launch_bucket_reduce<KT, 1, 2>(ctx, K, A);
-    else if (nl == 2) launch_bucket_reduce<KT, 2, 2>(ctx, K, A);
-    else launch_bucket_reduce<KT, 3, 2>(ctx, K, A);
-  }
-  LAUNCHED(1);
-  CUDA_TRY(cudaGetLastError());
-  ctx.tm.mark(7, "bucket_reduce");
-  unsigned long long nnz;
-  uint32_t ovf;
-  CUDA_TRY(cudaMemcpyAsync(&nnz, sctr, 8, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaMemcpyAsync(&ovf, flags + 1, 4, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  if (getenv("PGPU_DEBUG"))
-    fprintf(stderr, "[pgpu] bucket terms=%llu staging=%llu overflow=%u\n", nnz,
-            (unsigned long long)scap, ovf);
-  if (ovf) return PGPU_OK;  // a large bin's key window exceeds the table: sort path
-  uint64_t* boff;
-  uint64_t* part64;
-  TRY(ctx.ar->alloc(&boff, K));
-  TRY(ctx.ar->alloc(&part64, kMaxScanBlocks + 1));
-  LAUNCHED(device_scan<uint64_t>(K, BnnzGen{bnnz}, BoffOut{boff}, part64, &g, ctx.st));
-  uint64_t *cexp, *ccoef;
-  TRY(outer->alloc_out(&cexp, nnz));
-  TRY(outer->alloc_out(&ccoef, (size_t)nnz * nl));
-  k_bucket_gather<<<K, 256, 0, ctx.st>>>(bbase, bnnz, boff, sexp, scoef, nl, cexp, ccoef);
-  LAUNCHED(1);
-  ctx.tm.mark(4, "compact");
-  out->exps = cexp;
-  out->coef = ccoef;
-  out->n = nnz;
-  *done = true;
-  return PGPU_OK;
-}
-
-template <typename KT>
-int bucket_range(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint64_t pairs, Slice* out,
-                 bool* done) {
-  Arena* outer = ctx.ar;
-  Arena batch(ctx.st, pairs * 48 < (64ull << 20) ? outer->dev : nullptr, outer->used);
-  ctx.ar = &batch;
-  int r = bucket_range_impl<KT>(ctx, outer, pb, KL, KH, pairs, out, done);
-  ctx.ar = outer;
-  return r;
-}
+// Bucket path driver (kernels in bucket_path.cuh)
+#include "bucket_driver.inc"
 
 template <typename KT>
 int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice>& slices,
@@ -1059,104 +588,8 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   return PGPU_OK;
 }
 
-// Small products (<= kSmallPairs pairs): one CTA, one launch, one round trip.
-// Returns PGPU_OK with *done = false when the product does not qualify.
-template <typename KT, int NL, int CK>
-void launch_small(Ctx& ctx, const SmallArgs& A) {
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(k_small_product<KT, NL, CK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)kSmallSmem);
-    attr = true;
-  }
-  k_small_product<KT, NL, CK><<<1, kSmallThreads, kSmallSmem, ctx.st>>>(A);
-}
-
-template <typename KT>
-void launch_small_kind(Ctx& ctx, const Problem& pb, const SmallArgs& A) {
-  const int nl = pb.nl ? pb.nl : 1;
-  if (pb.ck == PGPU_F64) launch_small<KT, 1, 0>(ctx, A);
-  else if (pb.ck == PGPU_I64) {
-    if (nl == 1) launch_small<KT, 1, 1>(ctx, A);
-    else if (nl == 2) launch_small<KT, 2, 1>(ctx, A);
-    else launch_small<KT, 3, 1>(ctx, A);
-  } else {
-    if (nl == 1) launch_small<KT, 1, 2>(ctx, A);
-    else if (nl == 2) launch_small<KT, 2, 2>(ctx, A);
-    else launch_small<KT, 3, 2>(ctx, A);
-  }
-}
-
-int small_run(Ctx& ctx, const Problem& pb, const pgpu_options& o, pgpu_result* out, bool* done) {
-  *done = false;
-  const uint64_t pairs = (uint64_t)pb.na * pb.nb;
-  if (pairs == 0 || pairs > (uint64_t)kSmallPairs) return PGPU_OK;
-  const int pbits = std::max(1, bitlen64(pairs - 1));
-  if (pb.P.kbits + pbits > 63) return PGPU_OK;
-  const int nl = pb.nl ? pb.nl : 1;
-  Arena& ar = *ctx.ar;
-  uint64_t *oexp, *ocoef;
-  unsigned long long* cnt;
-  if (o.outputs_on_device) {
-    TRY(ar.alloc_out(&oexp, pairs));
-    TRY(ar.alloc_out(&ocoef, pairs * nl));
-  } else {
-    TRY(ar.alloc(&oexp, pairs));
-    TRY(ar.alloc(&ocoef, pairs * nl));
-  }
-  TRY(ar.alloc(&cnt, 2));
-  SmallArgs A;
-  A.ak = pb.ak;
-  A.bk = pb.bk;
-  A.ac = pb.acoef;
-  A.bc = pb.bcoef;
-  A.na = pb.na;
-  A.nb = pb.nb;
-  A.KL = pb.KL;
-  A.KH = pb.KH;
-  A.pbits = pbits;
-  A.P = pb.P;
-  A.oexp = oexp;
-  A.ocoef = ocoef;
-  A.count = cnt;
-  if (pb.k32) launch_small_kind<uint32_t>(ctx, pb, A);
-  else launch_small_kind<uint64_t>(ctx, pb, A);
-  LAUNCHED(1);
-  CUDA_TRY(cudaGetLastError());
-  ctx.tm.mark(1, "small");
-  out->acc_limbs = nl;
-  out->path_used = PGPU_PATH_SMALL;
-  unsigned long long n = 0, formed = 0;
-  if (o.outputs_on_device) {
-    unsigned long long hc[2];
-    CUDA_TRY(cudaMemcpyAsync(hc, cnt, 16, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaStreamSynchronize(ctx.st));
-    n = hc[0];
-    formed = hc[1];
-    ar.release(oexp);
-    ar.release(ocoef);
-    out->exps = oexp;
-    out->coeffs = ocoef;
-  } else {
-    // capacity-sized copies ride along with the count: one round trip
-    out->exps = (uint64_t*)g_pinned.get(pairs * 8 + 64);  // + the two counters
-    out->coeffs = g_pinned.get(pairs * 8 * nl);
-    out->_owner = (void*)kPinnedTag;
-    if (!out->exps || !out->coeffs) return fail(PGPU_ENOMEM, "pinned host allocation failed");
-    unsigned long long* hcnt = reinterpret_cast<unsigned long long*>(out->exps + pairs);
-    CUDA_TRY(cudaMemcpyAsync(out->exps, oexp, pairs * 8, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(out->coeffs, ocoef, pairs * 8 * nl, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(hcnt, cnt, 16, cudaMemcpyDeviceToHost, ctx.st));
-    CUDA_TRY(cudaStreamSynchronize(ctx.st));
-    n = hcnt[0];
-    formed = hcnt[1];
-  }
-  out->n = (int64_t)n;
-  out->pairs = (int64_t)formed;
-  ctx.tm.mark(5, "output");
-  *done = true;
-  return PGPU_OK;
-}
+// Small-product driver (kernel in small_path.cuh)
+#include "small_driver.inc"
 
 int copy_in(Ctx& ctx, const pgpu_poly* p, size_t csz, const pgpu_options& o, const uint64_t** exps,
             const void** coef) {
@@ -1348,111 +781,8 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   return PGPU_OK;
 }
 
-// PolyFile text of terms [begin, end) (reference io.format_poly, io.py:241-248).
-int format_impl(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64_t end,
-                const pgpu_options* opt, pgpu_text* out) {
-  if (!p || !lay || !out) return fail(PGPU_EINVAL, "null argument");
-  memset(out, 0, sizeof *out);
-  pgpu_options o;
-  if (opt) o = *opt; else pgpu_default_options(&o);
-  out->on_device = o.outputs_on_device;
-  if (lay->nfields < 1 || lay->nfields > PGPU_MAX_FIELDS)
-    return fail(PGPU_EINVAL, "layout needs 1..%d fields", PGPU_MAX_FIELDS);
-  if (begin < 0 || end > p->n || begin > end)
-    return fail(PGPU_EINVAL, "term range [%lld, %lld) outside [0, %lld)", (long long)begin,
-                (long long)end, (long long)p->n);
-  text::LineSpec spec;
-  memset(&spec, 0, sizeof spec);
-  int coef_digits;
-  size_t csz;
-  if (o.coef_kind == PGPU_F64) {
-    spec.kind = 0;
-    spec.nl = 1;
-    coef_digits = 24;  // "-d.dddddddddddddddde-308"
-    csz = 8;
-  } else if (o.coef_kind == PGPU_I64 || o.coef_kind == PGPU_I128) {
-    spec.kind = 1;
-    spec.nl = o.coef_kind == PGPU_I128 ? 2 : (o.acc_limbs ? o.acc_limbs : 1);
-    if (spec.nl < 1 || spec.nl > 3) return fail(PGPU_EINVAL, "integer width must be 1..3 limbs");
-    coef_digits = 1 + (spec.nl == 1 ? 20 : spec.nl == 2 ? 39 : 58);
-    csz = 8 * (size_t)spec.nl;
-  } else {
-    return fail(PGPU_EINVAL, "unknown coefficient kind");
-  }
-  const int first = lay->order == PGPU_GRLEX ? 1 : 0;  // the grlex degree is not printed
-  spec.nvars = lay->nfields - first;
-  uint32_t maxline = (uint32_t)coef_digits + 1;
-  for (int f = 0; f < spec.nvars; ++f) {
-    const int w = lay->width[first + f];
-    spec.shift[f] = lay->shift[first + f];
-    spec.mask[f] = w >= 64 ? ~0ull : ((1ull << w) - 1);
-    uint64_t m = spec.mask[f];
-    int d = 1;
-    while (m >= 10) {
-      m /= 10;
-      ++d;
-    }
-    maxline += 1 + (uint32_t)d;
-  }
-  const uint64_t n = (uint64_t)(end - begin);
-  if (n == 0) return PGPU_OK;
-
-  cudaStream_t lib_st;
-  TRY(device_setup(o.device, &lib_st));
-  Ctx ctx;
-  ctx.st = o.stream ? (cudaStream_t)o.stream : lib_st;
-  DeviceState& dstate = g_dev[o.device & 63];
-  std::lock_guard<std::mutex> ws_lock(dstate.mu);
-  TRY(grow_workspace(dstate, ctx.st));
-  Arena ar(ctx.st, &dstate);
-  ctx.ar = &ar;
-  const uint64_t* exps;
-  const void* coef;
-  if (o.inputs_on_device) {
-    exps = p->exps + begin;
-    coef = (const uint8_t*)p->coeffs + (size_t)begin * csz;
-  } else {
-    uint64_t* e;
-    uint8_t* c;
-    TRY(ar.alloc(&e, n));
-    TRY(ar.alloc(&c, n * csz));
-    CUDA_TRY(cudaMemcpyAsync(e, p->exps + begin, n * 8, cudaMemcpyHostToDevice, ctx.st));
-    CUDA_TRY(cudaMemcpyAsync(c, (const uint8_t*)p->coeffs + (size_t)begin * csz, n * csz,
-                             cudaMemcpyHostToDevice, ctx.st));
-    exps = e;
-    coef = c;
-  }
-  uint64_t* offs;
-  uint64_t* part;
-  TRY(ar.alloc(&offs, n + 1));
-  TRY(ar.alloc(&part, kMaxScanBlocks + 1));
-  int g = 0;
-  device_scan<uint64_t>(n, FmtLen{exps, coef, spec}, FmtOff{offs, n}, part, &g, ctx.st);
-  uint64_t total = 0;
-  CUDA_TRY(cudaMemcpyAsync(&total, offs + n, 8, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  char* dtext;
-  if (o.outputs_on_device) TRY(ar.alloc_out(&dtext, total));
-  else TRY(ar.alloc(&dtext, total));
-  const size_t smem = (size_t)kFmtThreads * maxline;
-  if (smem > 48 * 1024)
-    CUDA_TRY(cudaFuncSetAttribute(k_fmt_write, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  const uint64_t blocks = (n + kFmtThreads - 1) / kFmtThreads;
-  k_fmt_write<<<(unsigned)blocks, kFmtThreads, smem, ctx.st>>>(exps, coef, spec, n, offs, dtext);
-  CUDA_TRY(cudaGetLastError());
-  if (o.outputs_on_device) {
-    ar.release(dtext);
-    out->text = dtext;
-  } else {
-    out->text = (char*)g_pinned.get(std::max<uint64_t>(total, 1));
-    if (!out->text) return fail(PGPU_ENOMEM, "pinned host allocation failed");
-    out->_owner = (void*)kPinnedTag;
-    CUDA_TRY(cudaMemcpyAsync(out->text, dtext, total, cudaMemcpyDeviceToHost, ctx.st));
-  }
-  out->bytes = (int64_t)total;
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  return PGPU_OK;
-}
+// PolyFile formatter driver (kernels in format.cuh, text.cuh)
+#include "format_driver.inc"
 
 }  // namespace
 
