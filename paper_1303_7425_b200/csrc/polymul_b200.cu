@@ -277,6 +277,8 @@ struct Timer {
 struct Ctx {
   cudaStream_t st;
   Arena* ar;
+  void* rh_key = nullptr;     // row hash of operand a (sort path j-records: RowSlot<KT>[]), or null
+  uint32_t rh_mask = 0;
   uint8_t* batch_blk = nullptr;  // one block reused by every batch of a product
   size_t batch_cap = 0;
   size_t mem_budget = 0;  // bytes this call may plan to use for large scratch
@@ -393,6 +395,29 @@ int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice
     if ((span >> 32) <= 48 && !getenv("PGPU_NO_SPAN32")) max_span = 0xffffffffull;
   }
   TRY(plan_batches<KT>(ctx, pb, pb.KL, pb.KH, total, cap, ranges, counts, max_span));
+  // Large products: 8-byte sort records (key, column j); the row of a pair is
+  // recovered from its key through a hash of operand a's keys, built once here.
+  // (Keys of a are distinct; the all-ones key marks empty slots, so it must be
+  // out of range.)
+  ctx.rh_key = nullptr;
+  const uint64_t jrec_min = getenv("PGPU_JREC_MIN") ? strtoull(getenv("PGPU_JREC_MIN"), nullptr, 10)
+                                                   : (1ull << 20);
+  if (total >= jrec_min && pb.P.kbits < (int)(8 * sizeof(KT)) && !getenv("PGPU_NO_JREC")) {
+    uint32_t cap = 1;
+    while (cap < 2 * pb.na) cap <<= 1;
+    RowSlot<KT>* slots;
+    TRY(ctx.ar->alloc(&slots, cap));
+    CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(RowSlot<KT>) * cap, ctx.st));
+    k_row_hash_build<KT><<<grid_for(pb.na, 256, 1 << 30), 256, 0, ctx.st>>>((const KT*)pb.ak, pb.na, slots,
+                                                                          cap - 1);
+    LAUNCHED(1);
+    ctx.rh_key = slots;
+    ctx.rh_mask = cap - 1;
+  }
+  struct RowHashOff {
+    Ctx& c;
+    ~RowHashOff() { c.rh_key = nullptr; }
+  } rh_off{ctx};
   // Products with several large batches: one scratch block sized for the
   // largest batch serves them all (per-batch pool allocations of tens of GB
   // made run times vary by up to 2x through physical remapping).

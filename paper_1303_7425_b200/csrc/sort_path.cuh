@@ -44,6 +44,79 @@ k_gen(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __re
   }
 }
 
+// K1 with 32-bit records: the value is the column j only.  The row is
+// recovered in K4 from the key: a_i = key + KL - b_j, looked up in a hash of
+// the operand a keys (keys of a are distinct).  12 -> 8 bytes per record
+// through every radix pass.
+template <typename KT, typename RT>
+__global__ void __launch_bounds__(256)
+k_gen_j(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
+        const uint32_t* __restrict__ rhi, const uint64_t* __restrict__ off, uint32_t na,
+        uint64_t KL, RT* __restrict__ keys, uint32_t* __restrict__ vals) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nwarps) {
+    uint32_t j0 = rlo[i], j1 = rhi[i];
+    if (j0 >= j1) continue;
+    uint64_t base = off[i] - j0;
+    uint64_t ai = (uint64_t)ak[i] - KL;
+    for (uint32_t j = j0 + lane; j < j1; j += 32) {
+      keys[base + j] = (RT)(ai + (uint64_t)__ldg(bk + j));
+      vals[base + j] = j;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t row_hash(uint64_t k) {
+  return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> 32);
+}
+__device__ __forceinline__ uint32_t cas_row(uint32_t* p, uint32_t cmp, uint32_t v) {
+  return atomicCAS(reinterpret_cast<unsigned int*>(p), cmp, v);
+}
+__device__ __forceinline__ uint64_t cas_row(uint64_t* p, uint64_t cmp, uint64_t v) {
+  return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp,
+                   (unsigned long long)v);
+}
+
+// open-addressing table key -> row of operand a (empty slot: all-ones key);
+// key and row share one slot so a probe is a single load
+template <typename KT>
+struct alignas(2 * sizeof(KT)) RowSlot {
+  KT key;
+  uint32_t row;
+};
+
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_row_hash_build(const KT* __restrict__ ak, uint32_t na, RowSlot<KT>* __restrict__ slots, uint32_t mask) {
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= na) return;
+  const KT key = ak[i];
+  uint32_t h = row_hash((uint64_t)key) & mask;
+  for (;;) {
+    const KT prev = cas_row(&slots[h].key, (KT)~(KT)0, key);
+    if (prev == (KT)~(KT)0) {
+      slots[h].row = i;
+      return;
+    }
+    h = (h + 1) & mask;
+  }
+}
+
+template <typename KT>
+struct RowHash {
+  const RowSlot<KT>* slots;
+  uint32_t mask;
+  __device__ __forceinline__ uint32_t find(uint64_t key) const {
+    uint32_t h = row_hash(key) & mask;
+    for (;;) {
+      const RowSlot<KT> e = slots[h];
+      if ((uint64_t)e.key == key) return e.row;
+      h = (h + 1) & mask;
+    }
+  }
+};
+
 // ---- K2: LSD radix sort (onesweep) ------------------------------------------
 // One upfront histogram kernel gives every pass's global digit counts (the
 // multiset of keys is the same for all passes).  Each pass is then a single
@@ -126,14 +199,17 @@ __global__ void __launch_bounds__(kRsDigits) k_rs_hist_scan(unsigned int* ghist,
   }
 }
 
-template <typename KT>
-__global__ void __launch_bounds__(kRsThreads, PGPU_RS_MINB)
-k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* __restrict__ kout,
-              uint64_t* __restrict__ vout, uint64_t n, int shift, const unsigned int* __restrict__ gbase,
+#ifndef PGPU_RS_MINB32
+#define PGPU_RS_MINB32 4
+#endif
+template <typename KT, typename VT = uint64_t>
+__global__ void __launch_bounds__(kRsThreads, sizeof(VT) == 4 ? PGPU_RS_MINB32 : PGPU_RS_MINB)
+k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restrict__ kout,
+              VT* __restrict__ vout, uint64_t n, int shift, const unsigned int* __restrict__ gbase,
               unsigned long long* status, unsigned int* tile_ctr) {
   extern __shared__ __align__(16) uint8_t rs_smem[];
-  KT* skey = reinterpret_cast<KT*>(rs_smem);                                   // [kRsTile]
-  uint64_t* sval = reinterpret_cast<uint64_t*>(rs_smem + sizeof(KT) * kRsTile);  // [kRsTile]
+  VT* sval = reinterpret_cast<VT*>(rs_smem);                                   // [kRsTile]
+  KT* skey = reinterpret_cast<KT*>(rs_smem + sizeof(VT) * kRsTile);            // [kRsTile]
   __shared__ uint32_t wcnt[kRsWarps][kRsDigits];
   __shared__ uint32_t tstart[kRsDigits];
   __shared__ uint32_t ttot[kRsDigits];
@@ -149,7 +225,7 @@ k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* 
   const uint64_t t0 = (uint64_t)t * kRsTile;
   const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
   KT key[kRsIpt];
-  uint64_t val[kRsIpt];
+  VT val[kRsIpt];
   uint32_t rank[kRsIpt];
   unsigned dig[kRsIpt];
   // warp w owns tile items [w*512, (w+1)*512): warp-major order is input order
@@ -158,7 +234,7 @@ k_rs_onesweep(const KT* __restrict__ kin, const uint64_t* __restrict__ vin, KT* 
     const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
     const bool ok = idx < end;
     key[k] = ok ? kin[idx] : KT(0);
-    val[k] = ok ? vin[idx] : 0ull;
+    val[k] = ok ? vin[idx] : VT(0);
   }
 #pragma unroll
   for (int k = 0; k < kRsIpt; ++k) {
@@ -327,6 +403,67 @@ k_seg_reduce_f64(const KT* __restrict__ keys, const uint64_t* __restrict__ vals,
     acc = __dadd_rn(acc, __dmul_rn(__ldg(ac + (v >> 32)), __ldg(bc + (v & 0xffffffffu))));
   }
   oexp[s] = expand_key((uint64_t)keys[p0] + KL, P);
+  ocoef[s] = acc;
+  onz[s] = (acc != 0.0) ? 1u : 0u;  // NaN != 0 -> kept, +-0 dropped (merge.py:63)
+}
+
+// K4 on j-records: the segment's key gives every pair's row through the hash
+// (a_i = key + KL - b_j), then the same folds as above.
+template <typename KT, typename RT, int NL, int CK, int G>
+__global__ void __launch_bounds__(256)
+k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ vals,
+                   const uint32_t* __restrict__ starts, uint32_t nseg, const KT* __restrict__ bk,
+                   RowHash<KT> rows, const void* __restrict__ ac, const void* __restrict__ bc, uint64_t KL,
+                   KeyPlan P, uint64_t* __restrict__ oexp, uint64_t* __restrict__ ocoef,
+                   uint32_t* __restrict__ onz) {
+  const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const uint32_t g = threadIdx.x % G;
+  const bool live = s < nseg;
+  const uint32_t p0 = live ? starts[s] : 0u, p1 = live ? starts[s + 1] : 0u;
+  const uint64_t key = live ? (uint64_t)keys[p0] + KL : 0ull;
+  Limbs<NL> acc;
+  limbs_zero(acc);
+  for (uint32_t p = p0 + g; p < p1; p += G) {
+    const uint32_t j = vals[p];
+    const uint32_t i = rows.find(key - (uint64_t)__ldg(bk + j));
+    limbs_add(acc, imul<NL, CK>(load_icoef<CK>(ac, (int64_t)i), load_icoef<CK>(bc, (int64_t)j)));
+  }
+  if constexpr (G > 1) {
+#pragma unroll
+    for (int d = G / 2; d >= 1; d >>= 1) {
+      Limbs<NL> o;
+#pragma unroll
+      for (int k = 0; k < NL; ++k) o.w[k] = __shfl_down_sync(0xffffffffu, acc.w[k], d, G);
+      limbs_add(acc, o);
+    }
+  }
+  if (!live || g != 0) return;
+  oexp[s] = expand_key(key, P);
+#pragma unroll
+  for (int k = 0; k < NL; ++k) ocoef[(uint64_t)s * NL + k] = acc.w[k];
+  onz[s] = limbs_nonzero(acc) ? 1u : 0u;
+}
+
+template <typename KT, typename RT>
+__global__ void __launch_bounds__(256)
+k_seg_reduce_f64_j(const RT* __restrict__ keys, const uint32_t* __restrict__ vals,
+                   const uint32_t* __restrict__ starts, uint32_t nseg, const KT* __restrict__ bk,
+                   RowHash<KT> rows, const double* __restrict__ ac, const double* __restrict__ bc,
+                   uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp, double* __restrict__ ocoef,
+                   uint32_t* __restrict__ onz) {
+  uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const uint32_t p0 = starts[s], p1 = starts[s + 1];
+  const uint64_t key = (uint64_t)keys[p0] + KL;
+  // reference order: the stable sort kept generation order, i.e. increasing i
+  double acc = 0.0;
+  for (uint32_t p = p0; p < p1; ++p) {
+    const uint32_t j = vals[p];
+    const uint32_t i = rows.find(key - (uint64_t)__ldg(bk + j));
+    const double pr = __dmul_rn(__ldg(ac + i), __ldg(bc + j));
+    acc = p == p0 ? pr : __dadd_rn(acc, pr);
+  }
+  oexp[s] = expand_key(key, P);
   ocoef[s] = acc;
   onz[s] = (acc != 0.0) ? 1u : 0u;  // NaN != 0 -> kept, +-0 dropped (merge.py:63)
 }

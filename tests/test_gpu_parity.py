@@ -414,3 +414,13 @@ def test_concurrent_callers_share_the_device():
     for t in threads:
         t.join()
     assert not errors, errors
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_golden_cases_sort_path_column_records(case, monkeypatch):
+    """The sort path's 8-byte records (key, column j; the row recovered through
+    the hash of operand a's keys), forced on every golden case."""
+    monkeypatch.setenv("PGPU_JREC_MIN", "1")
+    name, a, b, split, want = case
+    got = mul(a, b, MulConfig(path="sort", float_ordered=True), split=None if split is None else SplitSet(split))
+    _check(got, want)
