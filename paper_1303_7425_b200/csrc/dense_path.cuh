@@ -197,6 +197,9 @@ constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot t
 constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
 constexpr size_t kAccBytes = 80 * 1024;
 constexpr int kUnroll = PGPU_UNROLL;       // independent columns per lane per step
+#ifndef PGPU_ROW_SELECT
+#define PGPU_ROW_SELECT 1
+#endif
 #ifndef PGPU_ROW_CLAIM
 #define PGPU_ROW_CLAIM 32
 #endif
@@ -516,11 +519,18 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
             c += nv;
             if (nv < 32u * kUnroll) break;
           }
+#if PGPU_ROW_SELECT
+          // branch-free: every lane computes, the row's owner keeps it
+          const KT nxt = c < nb ? (KT)(akr + __ldg(bk + (c < nb ? c : 0))) : kInf;
+          ci = lane == src ? c : ci;
+          nki = lane == src ? nxt : nki;
+#else
           if (lane == src) {
             ci = c;
             nki = c < nb ? (KT)(akr + bk[c]) : kInf;
           }
           __syncwarp();
+#endif
         }
         if (rowok) {
           cur[i] = ci;
