@@ -195,7 +195,10 @@ constexpr int kNumWarps = PGPU_NUM_WARPS;
 constexpr int kNumThreads = kNumWarps * 32;
 constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot table
 constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
-constexpr size_t kAccBytes = 80 * 1024;
+#ifndef PGPU_ACC_KB
+#define PGPU_ACC_KB 80
+#endif
+constexpr size_t kAccBytes = PGPU_ACC_KB * 1024;
 constexpr int kUnroll = PGPU_UNROLL;       // independent columns per lane per step
 #ifndef PGPU_ROW_SELECT
 #define PGPU_ROW_SELECT 1
