@@ -463,17 +463,20 @@ k_bucket_reduce(BucketArgs A) {
 }
 
 // ---- B5: bucket runs -> final order -------------------------------------------
+// One warp per bucket (runs average tens of terms; a CTA per bucket left most
+// of its threads idle).
 __global__ void __launch_bounds__(256)
 k_bucket_gather(const uint64_t* __restrict__ bbase, const uint32_t* __restrict__ bnnz,
                 const uint64_t* __restrict__ boff, const uint64_t* __restrict__ sexp,
-                const uint64_t* __restrict__ scoef, int nl, uint64_t* __restrict__ oexp,
+                const uint64_t* __restrict__ scoef, int nl, uint32_t nbuckets, uint64_t* __restrict__ oexp,
                 uint64_t* __restrict__ ocoef) {
-  const uint32_t k = blockIdx.x;
+  const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (k >= nbuckets) return;
   const uint32_t n = bnnz[k];
   const uint64_t src = bbase[k], dst = boff[k];
-  for (uint32_t t = threadIdx.x; t < n; t += blockDim.x) oexp[dst + t] = sexp[src + t];
-  for (uint32_t t = threadIdx.x; t < n * (uint32_t)nl; t += blockDim.x)
-    ocoef[dst * nl + t] = scoef[src * nl + t];
+  for (uint32_t t = lane; t < n; t += 32) oexp[dst + t] = sexp[src + t];
+  for (uint32_t t = lane; t < n * (uint32_t)nl; t += 32) ocoef[dst * nl + t] = scoef[src * nl + t];
 }
 
 // bin offsets (exclusive scan of the fine-bin histogram)
