@@ -3,27 +3,30 @@
 // The sort path moves every pair record through the global radix sort (one
 // histogram pass plus 4-5 read+write passes).  For sparse products such as
 // Monagan-Pearce most of that traffic is avoidable: an output term only needs
-// its own pairs, and a paper interval of a few thousand pairs fits in one
-// CTA's shared memory.  So the key range is cut into *buckets* of at most
+// its own pairs, and a paper interval of a few hundred pairs fits in one
+// CTA's shared memory.  So the key range is cut into *buckets* of fewer than
 // kBucketCap pairs (paper intervals sized for a CTA, split.py:1-9: equal keys
 // never straddle a bound) and
 //
-//   B1 k_bin_count    every pair's fine bin ((key - KL) >> s), counted with
-//                     one atomic per run of equal bins in a warp (keys ascend
-//                     along a row, so a warp's bins form runs)
-//   B2 device_scan    bin offsets; bucket(bin) = offset / (cap/2), so a bucket
-//                     is a run of bins holding < cap pairs (every bin <= cap/2)
+//   B1 k_bin_count ×2 fine bins: coarse bins of 2^s1 keys, each split into 2^r
+//                     equal sub-bins of ~kBinTarget pairs (BinMap); counted
+//                     with one atomic per run of equal bins in a warp (keys
+//                     ascend along a row, so a warp's bins form runs)
+//   B2 device_scan    bin offsets; buckets = runs of bins whose offsets share a
+//                     window of kBucketHalf records, a larger bin on its own
 //   B3 k_bin_scatter  the same walk writes (key - KL, i<<32|j) once, at
 //                     offset(bin) + atomic run position: records of one bucket
 //                     are contiguous
-//   B4 k_bucket_reduce one CTA per bucket: records -> shared-memory hash of
-//                     keys (slot per record), distinct keys bitonic-sorted,
-//                     records counting-sorted by key rank, one owner thread
-//                     per term sums its pairs' products (exact limbs, or f64
-//                     in fast mode), zero sums dropped (merge.py:63), terms
-//                     appended to a staging area
-//   B5 k_bucket_gather bucket term runs -> final positions (bucket order =
-//                     key order)
+//   B4 k_bucket_reduce one CTA per bucket: coalesced record loads and
+//                     coefficient products; keys hashed into a shared-memory
+//                     table whose slots accumulate the exact sums (32-bit
+//                     atomics with explicit carries; f64 atomics in fast
+//                     mode); distinct keys ranked (counting rank, or bitonic
+//                     above 256); nonzero terms (merge.py:63) appended to a
+//                     staging run.  A bucket that is one large bin is reduced
+//                     in dense mode over the bin's key window.
+//   B5 k_bucket_gather bucket runs -> final positions (bucket order = key
+//                     order), one warp per bucket
 //
 // DRAM traffic per pair: one record write + one record read (12-16 B each),
 // against 5-6 read+write passes on the sort path.  The float-ordered mode
