@@ -13,6 +13,10 @@
 //   K4 seg reduce   one thread owns one output term and folds its segment in
 //                   order (acc = p_first; acc += p ...), merge.py:49-58
 //   K5 nz compact   drop zero sums (merge.py:63)
+//
+// Products of 2^20 pairs or more use 8-byte records (local key, column j):
+// k_gen_j writes them, K4 recovers each pair's row from its key through a
+// hash of operand a's keys (k_seg_reduce_*_j).
 #pragma once
 #include "common.cuh"
 #include "scan.cuh"
