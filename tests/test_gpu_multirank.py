@@ -28,7 +28,7 @@ def _port():
 
 @pytest.mark.parametrize("ranks,config,gather", [(2, "fateman10", "peer"), (3, "fateman20", "peer"),
                                                  (2, "mp12", "peer"), (2, "fateman10", "collective"),
-                                                 (3, "mp12", "collective")])
+                                                 (3, "mp12", "collective"), (8, "mp12", "peer")])
 def test_emulated_ranks_reproduce_reference_digest(ranks, config, gather):
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={ranks}",
            "--master-addr", "127.0.0.1", f"--master-port={_port()}", str(ROOT / "bench.py"),
