@@ -53,9 +53,11 @@ def parse():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    ap.add_argument("--config", default="fateman30")
+    ap.add_argument("--config", default="fateman30",
+                    help="workload: fateman10 | fateman20 | fateman30 | mp12 | mp25 (BASELINE.json configs)")
     ap.add_argument("--coeff", choices=["int", "float"], default="int")
-    ap.add_argument("--path", default="auto")
+    ap.add_argument("--path", default="auto",
+                    help="device algorithm: auto | dense | bucket | sort | small (pgpu_options.path)")
     ap.add_argument("--gather", default="peer", choices=("peer", "collective"),
                     help="N>1: assemble the slices by peer copies (CUDA IPC) or an all-gather")
     ap.add_argument("--flush-mib", type=int, default=512)
