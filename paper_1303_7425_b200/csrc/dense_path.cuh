@@ -42,22 +42,40 @@
 namespace pgpu {
 
 // ---- D1 ---------------------------------------------------------------------
-// Tiles of kSymRows x kSymCols pairs.  A tile's keys lie in
-// [ak[r0]+bk[c0], ak[r1-1]+bk[c1-1]]; when that window fits kSymWin bytes the
-// tile first marks a shared-memory bytemap (deduplicating the ~16x repeated
-// keys of dense operands) and then writes only the marked bytes to the global
-// bytemap.  Wider tiles store straight to global memory.  Stores are
-// idempotent byte writes of 1: no atomics, independent of order.
+// Tiles of kSymRows x kSymCols pairs.  A tile is cut into sub-tiles whose key
+// window fits kSymWin bytes: column segments of span < kSymWin/2, then row
+// segments filling the rest (a single row or column has span 0, so every
+// sub-tile fits; the operands are sorted, so segment ends are found by binary
+// search).  A sub-tile marks a shared-memory bytemap over its window
+// (deduplicating the ~16x repeated keys of dense operands) and ORs the marked
+// words into the global bytemap.  Marks are idempotent byte writes of 1: no
+// atomics on per-pair data, independent of order.
 #ifndef PGPU_SYM_UNROLL
 #define PGPU_SYM_UNROLL 4
 #endif
 constexpr int kSymUnroll = PGPU_SYM_UNROLL;
-constexpr int kSymRows = 64;
+#ifndef PGPU_SYM_ROWS
+#define PGPU_SYM_ROWS 256
+#endif
+constexpr int kSymRows = PGPU_SYM_ROWS;
 constexpr int kSymCols = 256;
 #ifndef PGPU_SYM_WIN
-#define PGPU_SYM_WIN 65536
+#define PGPU_SYM_WIN 49152
 #endif
 constexpr uint32_t kSymWin = PGPU_SYM_WIN;
+
+// largest e in (from, to] with s[e-1] - s[from] <= lim (s ascending)
+template <typename KT>
+__device__ __forceinline__ uint32_t sym_seg_end(const KT* s, uint32_t from, uint32_t to, uint64_t lim) {
+  const uint64_t k0 = s[from];
+  uint32_t lo = from + 1, hi = to;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi + 1) >> 1;
+    if ((uint64_t)s[mid - 1] - k0 <= lim) lo = mid;
+    else hi = mid - 1;
+  }
+  return lo;
+}
 
 template <typename KT>
 __global__ void __launch_bounds__(256)
@@ -66,7 +84,7 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
            uint8_t* __restrict__ bytemap) {
   extern __shared__ __align__(16) uint8_t win[];  // kSymWin bytes
   __shared__ KT sb[kSymCols];
-  __shared__ KT sa[kSymRows];
+  __shared__ __align__(16) KT sa[kSymRows];
   __shared__ uint32_t slo[kSymRows], shi[kSymRows];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t ntr = (na + kSymRows - 1) / kSymRows, ntc = (nb + kSymCols - 1) / kSymCols;
@@ -78,57 +96,76 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
     // rows' column ranges shrink leftwards with i: the tile is empty unless
     // [rlo[r1-1], rhi[r0]) meets [c0, c1)
     if (rhi[r0] <= c0 || rlo[r1 - 1] >= c1) continue;
-    // window aligned to 16 keys (relative to R0) so the flush can OR whole words
-    const uint64_t wlo = R0 + (((uint64_t)ak[r0] + (uint64_t)bk[c0] - R0) & ~15ull);
-    const uint64_t whi = (uint64_t)ak[r1 - 1] + (uint64_t)bk[c1 - 1];
-    const bool local = whi - wlo < kSymWin;
-    const uint32_t wn = local ? (uint32_t)(whi - wlo + 1) : 0u;
     for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) sb[c - c0] = bk[c];
     for (uint32_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
       sa[i - r0] = ak[i];
-      slo[i - r0] = max(rlo[i], c0);
-      shi[i - r0] = min(rhi[i], c1);
+      slo[i - r0] = rlo[i];
+      shi[i - r0] = rhi[i];
     }
-    if (local)
-      for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x)
-        reinterpret_cast<uint4*>(win)[q] = make_uint4(0, 0, 0, 0);
     __syncthreads();
-    // every row spans the tile's whole column range (rlo is non-increasing in
-    // the row, rhi too): thread t owns column c0+t for all rows, so a mark is
-    // one broadcast shared load, an add and a byte store
-    const bool full = local && rlo[r0] <= c0 && rhi[r1 - 1] >= c1 && (c1 - c0) == (uint32_t)kSymCols &&
-                      blockDim.x == (unsigned)kSymCols;
-    if (full) {
-      const uint32_t boff = (uint32_t)((uint64_t)sb[threadIdx.x] - wlo);
+    for (uint32_t cs = 0; cs < c1 - c0;) {
+      const uint32_t ce = sym_seg_end(sb, cs, c1 - c0, kSymWin / 2 - 1);
+      const uint64_t bspan = (uint64_t)sb[ce - 1] - (uint64_t)sb[cs];
+      for (uint32_t rs = 0; rs < r1 - r0;) {
+        const uint32_t re = sym_seg_end(sa, rs, r1 - r0, kSymWin - 32 - bspan);
+        // window aligned to 16 keys (relative to R0) so the flush can OR whole
+        // words; marked keys are >= R0 (rows' column ranges), so clip there
+        const uint64_t kmin = max((uint64_t)sa[rs] + (uint64_t)sb[cs], R0);
+        const uint64_t wlo = R0 + ((kmin - R0) & ~15ull);
+        const uint32_t wn = (uint32_t)((uint64_t)sa[re - 1] + (uint64_t)sb[ce - 1] - wlo + 1);
+        const uint32_t gc0 = c0 + cs, gc1 = c0 + ce;
+        // rows of the sub-tile meeting its columns (rlo, rhi non-increasing in the row)
+        if (shi[rs] > gc0 && slo[re - 1] < gc1) {
+          for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x)
+            reinterpret_cast<uint4*>(win)[q] = make_uint4(0, 0, 0, 0);
+          __syncthreads();
+          if (slo[rs] <= gc0 && shi[re - 1] >= gc1) {
+            // every row spans every column: thread t owns column cs+t for all
+            // rows, so a mark is one broadcast shared load, an add and a byte store
+            if (threadIdx.x < ce - cs) {
+              const uint32_t boff = (uint32_t)((uint64_t)sb[cs + threadIdx.x] - wlo);
+              uint32_t i = rs;
+              if constexpr (sizeof(KT) == 4) {
+                // four rows' keys per broadcast LDS.128
+                for (; i < re && (i & 3); ++i) win[(uint32_t)sa[i] + boff] = 1;
+#pragma unroll 2
+                for (; i + 4 <= re; i += 4) {
+                  const uint4 k = *reinterpret_cast<const uint4*>(&sa[i]);
+                  win[k.x + boff] = 1;
+                  win[k.y + boff] = 1;
+                  win[k.z + boff] = 1;
+                  win[k.w + boff] = 1;
+                }
+              }
 #pragma unroll 8
-      for (uint32_t i = 0; i < r1 - r0; ++i) win[(uint32_t)sa[i] + boff] = 1;
-    }
-    for (uint32_t i = r0 + w; !full && i < r1; i += nw) {
-      const uint32_t lo = slo[i - r0], hi = shi[i - r0];
-      const uint64_t ai = sa[i - r0];
-      if (local) {
-        const uint32_t ao = (uint32_t)(ai + (uint64_t)bk[c0] - wlo);  // offset of column c0
-        const uint32_t b0 = (uint32_t)sb[0];
-        const uint32_t aob = ao - b0;  // window offset = aob + bk (mod 2^32; the sum is in range)
+              for (; i < re; ++i) win[(uint32_t)sa[i] + boff] = 1;
+            }
+          } else {
+            const uint32_t b0 = (uint32_t)sb[0];
+            for (uint32_t i = rs + w; i < re; i += nw) {
+              const uint32_t lo = max(slo[i], gc0), hi = min(shi[i], gc1);
+              const uint32_t ao = (uint32_t)((uint64_t)sa[i] + (uint64_t)sb[0] - wlo);
+              const uint32_t aob = ao - b0;  // window offset = aob + bk (mod 2^32; the sum is in range)
 #pragma unroll kSymUnroll
-        for (uint32_t j = lo + lane; j < hi; j += 32) win[aob + (uint32_t)sb[j - c0]] = 1;
-      } else {
-        const uint64_t a = ai - R0;
-        for (uint32_t j = lo + lane; j < hi; j += 32) bytemap[a + (uint64_t)sb[j - c0]] = 1;
+              for (uint32_t j = lo + lane; j < hi; j += 32) win[aob + (uint32_t)sb[j - c0]] = 1;
+            }
+          }
+          __syncthreads();
+          // OR the marked words into the global bytemap (other tiles set other bytes
+          // of the same words concurrently, so whole-word plain stores are not safe)
+          unsigned int* dst = reinterpret_cast<unsigned int*>(bytemap + (wlo - R0));
+          for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x) {
+            const uint4 v = reinterpret_cast<const uint4*>(win)[q];
+            if (v.x) atomicOr(dst + 4 * q, v.x);
+            if (v.y) atomicOr(dst + 4 * q + 1, v.y);
+            if (v.z) atomicOr(dst + 4 * q + 2, v.z);
+            if (v.w) atomicOr(dst + 4 * q + 3, v.w);
+          }
+          __syncthreads();
+        }
+        rs = re;
       }
-    }
-    __syncthreads();
-    if (local) {
-      // OR the marked words into the global bytemap (other tiles set other bytes
-      // of the same words concurrently, so whole-word plain stores are not safe)
-      unsigned int* dst = reinterpret_cast<unsigned int*>(bytemap + (wlo - R0));
-      for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x) {
-        const uint4 v = reinterpret_cast<const uint4*>(win)[q];
-        if (v.x) atomicOr(dst + 4 * q, v.x);
-        if (v.y) atomicOr(dst + 4 * q + 1, v.y);
-        if (v.z) atomicOr(dst + 4 * q + 2, v.z);
-        if (v.w) atomicOr(dst + 4 * q + 3, v.w);
-      }
+      cs = ce;
     }
     __syncthreads();
   }
