@@ -64,6 +64,17 @@ constexpr int kSymCols = 256;
 #endif
 constexpr uint32_t kSymWin = PGPU_SYM_WIN;
 
+#ifndef PGPU_SYM_SWZ
+#define PGPU_SYM_SWZ 1
+#endif
+// Window slot of window offset o.  Dense keys cluster in the low half of each
+// 64-key block of the lowest fields, so offsets 128 apart share banks; flipping
+// bit 5 by bit 7 moves every other pair of blocks to the unused banks.  The map
+// is an involution inside each aligned 64-byte block.
+__device__ __forceinline__ uint32_t sym_slot(uint32_t o) {
+  return PGPU_SYM_SWZ ? o ^ ((o >> 2) & 32u) : o;
+}
+
 // largest e in (from, to] with s[e-1] - s[from] <= lim (s ascending)
 template <typename KT>
 __device__ __forceinline__ uint32_t sym_seg_end(const KT* s, uint32_t from, uint32_t to, uint64_t lim) {
@@ -107,12 +118,13 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
       const uint32_t ce = sym_seg_end(sb, cs, c1 - c0, kSymWin / 2 - 1);
       const uint64_t bspan = (uint64_t)sb[ce - 1] - (uint64_t)sb[cs];
       for (uint32_t rs = 0; rs < r1 - r0;) {
-        const uint32_t re = sym_seg_end(sa, rs, r1 - r0, kSymWin - 32 - bspan);
+        const uint32_t re = sym_seg_end(sa, rs, r1 - r0, kSymWin - 128 - bspan);
         // window aligned to 16 keys (relative to R0) so the flush can OR whole
         // words; marked keys are >= R0 (rows' column ranges), so clip there
         const uint64_t kmin = max((uint64_t)sa[rs] + (uint64_t)sb[cs], R0);
         const uint64_t wlo = R0 + ((kmin - R0) & ~15ull);
-        const uint32_t wn = (uint32_t)((uint64_t)sa[re - 1] + (uint64_t)sb[ce - 1] - wlo + 1);
+        // bytes in use: the span rounded up to whole 64-byte swizzle blocks
+        const uint32_t wn = ((uint32_t)((uint64_t)sa[re - 1] + (uint64_t)sb[ce - 1] - wlo) + 64u) & ~63u;
         const uint32_t gc0 = c0 + cs, gc1 = c0 + ce;
         // rows of the sub-tile meeting its columns (rlo, rhi non-increasing in the row)
         if (shi[rs] > gc0 && slo[re - 1] < gc1) {
@@ -127,18 +139,18 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
               uint32_t i = rs;
               if constexpr (sizeof(KT) == 4) {
                 // four rows' keys per broadcast LDS.128
-                for (; i < re && (i & 3); ++i) win[(uint32_t)sa[i] + boff] = 1;
+                for (; i < re && (i & 3); ++i) win[sym_slot((uint32_t)sa[i] + boff)] = 1;
 #pragma unroll 2
                 for (; i + 4 <= re; i += 4) {
                   const uint4 k = *reinterpret_cast<const uint4*>(&sa[i]);
-                  win[k.x + boff] = 1;
-                  win[k.y + boff] = 1;
-                  win[k.z + boff] = 1;
-                  win[k.w + boff] = 1;
+                  win[sym_slot(k.x + boff)] = 1;
+                  win[sym_slot(k.y + boff)] = 1;
+                  win[sym_slot(k.z + boff)] = 1;
+                  win[sym_slot(k.w + boff)] = 1;
                 }
               }
 #pragma unroll 8
-              for (; i < re; ++i) win[(uint32_t)sa[i] + boff] = 1;
+              for (; i < re; ++i) win[sym_slot((uint32_t)sa[i] + boff)] = 1;
             }
           } else {
             const uint32_t b0 = (uint32_t)sb[0];
@@ -147,7 +159,7 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
               const uint32_t ao = (uint32_t)((uint64_t)sa[i] + (uint64_t)sb[0] - wlo);
               const uint32_t aob = ao - b0;  // window offset = aob + bk (mod 2^32; the sum is in range)
 #pragma unroll kSymUnroll
-              for (uint32_t j = lo + lane; j < hi; j += 32) win[aob + (uint32_t)sb[j - c0]] = 1;
+              for (uint32_t j = lo + lane; j < hi; j += 32) win[sym_slot(aob + (uint32_t)sb[j - c0])] = 1;
             }
           }
           __syncthreads();
@@ -156,10 +168,11 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
           unsigned int* dst = reinterpret_cast<unsigned int*>(bytemap + (wlo - R0));
           for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x) {
             const uint4 v = reinterpret_cast<const uint4*>(win)[q];
-            if (v.x) atomicOr(dst + 4 * q, v.x);
-            if (v.y) atomicOr(dst + 4 * q + 1, v.y);
-            if (v.z) atomicOr(dst + 4 * q + 2, v.z);
-            if (v.w) atomicOr(dst + 4 * q + 3, v.w);
+            const uint32_t lq = sym_slot(16 * q) / 16;  // the chunk's window offset / 16
+            if (v.x) atomicOr(dst + 4 * lq, v.x);
+            if (v.y) atomicOr(dst + 4 * lq + 1, v.y);
+            if (v.z) atomicOr(dst + 4 * lq + 2, v.z);
+            if (v.w) atomicOr(dst + 4 * lq + 3, v.w);
           }
           __syncthreads();
         }
