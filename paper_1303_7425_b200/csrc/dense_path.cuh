@@ -362,6 +362,11 @@ __device__ __forceinline__ void add_unsigned128(uint32_t* a, uint8_t* carry, uin
   if (cy) *carry += 1;
 }
 
+#ifndef PGPU_FOLD_ZERO
+#define PGPU_FOLD_ZERO 0
+#endif
+constexpr bool kFoldZero = PGPU_FOLD_ZERO;
+
 template <typename KT>
 __device__ __forceinline__ uint32_t rank_of(uint64_t klocal, const uint32_t* __restrict__ bits,
                                             const uint32_t* __restrict__ prefix) {
@@ -424,7 +429,9 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
     const uint32_t dcount = min(D, A.nout - base);
     const bool use_tbl = (Khi - Klo) <= kTbl;
     if (threadIdx.x == 0) row_ctr = 0;
-    for (uint32_t k = threadIdx.x; k < G::tbl_off / 4; k += blockDim.x) acc[k] = 0;
+    // the fold zeroes the copies it reads, so only a unit's first interval clears
+    if (!kFoldZero || t == t_begin)
+      for (uint32_t k = threadIdx.x; k < G::tbl_off / 4; k += blockDim.x) acc[k] = 0;
     if (use_tbl) {
       const uint64_t w0 = (Klo - A.R0) >> 5, w1 = (Khi - 1 - A.R0) >> 5;
       for (uint64_t wd = w0 + threadIdx.x; wd <= w1; wd += blockDim.x) {
@@ -602,6 +609,10 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
         double v = 0.0;
 #pragma unroll
         for (int q = 0; q < kNumWarps; ++q) v = __dadd_rn(v, dacc[q * DP + sl]);
+        if constexpr (kFoldZero) {
+#pragma unroll
+          for (int q = 0; q < kNumWarps; ++q) reinterpret_cast<double*>(acc)[q * DP + sl] = 0.0;
+        }
         if (A.R == 1) {
           reinterpret_cast<double*>(A.ocoef)[o] = v;
           A.onz[o] = v != 0.0 ? 1u : 0u;
@@ -635,6 +646,19 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
             cy = x >> 32;
           }
         }
+        if constexpr (kFoldZero) {
+#pragma unroll
+          for (int q = 0; q < kNumWarps; ++q) {
+            const uint32_t e = q * DP + sl;
+            if constexpr (CB) {
+              reinterpret_cast<ulonglong2*>(acc)[e] = make_ulonglong2(0ull, 0ull);
+              cbyte[e] = 0;
+            } else {
+#pragma unroll
+              for (int k = 0; k < NP; ++k) acc[k * STRIDE + e] = 0u;
+            }
+          }
+        }
         if (A.R == 1) {
           write_term<NW, MODE>(A, o, v);
         } else {
@@ -644,7 +668,9 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
         }
       }
     }
-    __syncthreads();
+    // with kFoldZero the next interval's table build needs no barrier here: the
+    // barrier after it orders this fold before the next interval's rows
+    if (!kFoldZero) __syncthreads();
   }
 }
 

@@ -12,4 +12,4 @@ timeout 900 python bench.py --config mp25 --steps 2 --warmup 1 --no-cpu-baseline
 KREGEX=k_numeric bash tools/gpu_prof.sh > gpurun_out/prof.log 2>&1
 nproc > gpurun_out/nproc.txt; lscpu | head -20 > gpurun_out/lscpu.txt
 tail -c 1500 gpurun_out/bench_full.log; tail -c 600 gpurun_out/bench_ref.log
-KREGEX=k_bucket_reduce CONFIG=mp12 bash tools/gpu_prof.sh > gpurun_out/prof_mp12.log 2>&1
+KREGEX=k_symbolic bash tools/gpu_prof.sh > gpurun_out/prof_sym.log 2>&1

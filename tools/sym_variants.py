@@ -18,8 +18,9 @@ from paper_1303_7425_b200.parmul import Operand
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="fateman30")
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--coeff", default="int")
 a = ap.parse_args()
-f, g = benchpolys.CONFIGS[a.config](int)
+f, g = benchpolys.CONFIGS[a.config](float if a.coeff == "float" else int)
 dev = torch.device("cuda", 0)
 A, B = DeviceOperand(Operand.from_poly(f), dev), DeviceOperand(Operand.from_poly(g), dev)
 st = torch.cuda.current_stream().cuda_stream
@@ -37,5 +38,5 @@ for k in range(2 + a.reps):
             acc.setdefault(n, []).append(v)
     r.free()
 med = {n: sorted(v)[len(v) // 2] for n, v in acc.items()}
-print("variant", Path(__import__("os").environ.get("PGPU_LIB", "default")).name, "digest", digest,
+print("variant", a.config, a.coeff, Path(__import__("os").environ.get("PGPU_LIB", "default")).name, "digest", digest,
       "total %.3f" % sum(med.values()), " ".join(f"{n}={v:.3f}" for n, v in med.items()), flush=True)
