@@ -42,7 +42,8 @@
 namespace pgpu {
 
 // ---- D1 ---------------------------------------------------------------------
-// Tiles of kSymRows x kSymCols pairs.  A tile is cut into sub-tiles whose key
+// Tiles of trows x kSymCols pairs (trows = kSymRows unless the product is too
+// small to fill the GPU with such tiles).  A tile is cut into sub-tiles whose key
 // window fits kSymWin bytes: column segments of span < kSymWin/2, then row
 // segments filling the rest (a single row or column has span 0, so every
 // sub-tile fits; the operands are sorted, so segment ends are found by binary
@@ -92,17 +93,17 @@ template <typename KT>
 __global__ void __launch_bounds__(256)
 k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
            const uint32_t* __restrict__ rhi, uint32_t na, uint32_t nb, uint64_t R0,
-           uint8_t* __restrict__ bytemap) {
+           uint8_t* __restrict__ bytemap, uint32_t trows) {  // trows <= kSymRows, multiple of 4
   extern __shared__ __align__(16) uint8_t win[];  // kSymWin bytes
   __shared__ KT sb[kSymCols];
   __shared__ __align__(16) KT sa[kSymRows];
   __shared__ uint32_t slo[kSymRows], shi[kSymRows];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const uint32_t ntr = (na + kSymRows - 1) / kSymRows, ntc = (nb + kSymCols - 1) / kSymCols;
+  const uint32_t ntr = (na + trows - 1) / trows, ntc = (nb + kSymCols - 1) / kSymCols;
   const uint64_t ntiles = (uint64_t)ntr * ntc;
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
     const uint32_t tr = (uint32_t)(tile % ntr), tc = (uint32_t)(tile / ntr);
-    const uint32_t r0 = tr * kSymRows, r1 = min(r0 + kSymRows, na);
+    const uint32_t r0 = tr * trows, r1 = min(r0 + trows, na);
     const uint32_t c0 = tc * kSymCols, c1 = min(c0 + kSymCols, nb);
     // rows' column ranges shrink leftwards with i: the tile is empty unless
     // [rlo[r1-1], rhi[r0]) meets [c0, c1)

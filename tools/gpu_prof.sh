@@ -11,4 +11,4 @@ if [ -n "$KREGEX" ]; then
   ncu --set full --clock-control none --import-source on -k regex:${KREGEX} -s ${SKIP:-0} -c 1 \
       -o gpurun_out/prof_${KREGEX}_${CONFIG:-fateman30} -f $CMD > gpurun_out/ncu_full.log 2>&1
 fi
-tail -3 gpurun_out/prof_plain.log; tail -3 gpurun_out/ncu_full.log
+tail -n 3 gpurun_out/prof_plain.log; tail -n 3 gpurun_out/ncu_full.log
