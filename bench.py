@@ -219,38 +219,96 @@ def cpu_sample(f, g, seconds_target, threads):
     return pairs / dt, desc, pairs, dt
 
 
+def python_reference_sample(f, g, threads, frac_den=64):
+    """The reference's own Python path (baseline/_ref, installed from
+    /root/reference by pip) on a contiguous 1/frac_den slice of its
+    select_grid(l=64) intervals: compute_intervals with its fork pool of
+    `threads` workers (parmul.py:64-88).  Returns a dict, or None when the
+    install is absent."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "polymul").exists():
+        return None
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        from polymul import core as rcore
+        from polymul import parmul as rparmul
+        from polymul import split as rsplit
+    except Exception as exc:  # pragma: no cover - install broken
+        return {"unavailable": f"import failed: {exc}"}
+    lay = rcore.default_layout(tuple(f.layout.vars.names), f.layout.order)
+    ra = rcore.Polynomial._from_sorted(lay, list(f.exps), list(f.coeffs), f.ctype)
+    rb = rcore.Polynomial._from_sorted(lay, list(g.exps), list(g.coeffs), g.ctype)
+    bounds = rsplit.select_grid(ra, rb, rsplit.GridParams(64)).bounds
+    n_int = len(bounds) - 1
+    width = max(1, n_int // frac_den)
+    start = (n_int - width) // 2
+    pairs = int(sum(rparmul.interval_op_counts(ra, rb, bounds, start, start + width)))
+    t0 = time.perf_counter()
+    rparmul.compute_intervals(ra, rb, bounds, start, start + width, "heap", threads)
+    dt = time.perf_counter() - t0
+    return {"value": pairs / dt, "unit": UNIT, "cores": threads, "kind": "reference",
+            "sample": f"intervals [{start}, {start + width}) of {n_int} select_grid(l=64) intervals "
+                      f"({pairs} of {f.n * g.n} term products), reference polymul.parmul."
+                      f"compute_intervals (heap merger, fork pool of {threads})",
+            "seconds": dt}
+
+
 def run_reference(args):
+    """The reference's CPU algorithm on the box's host cores: the oracle's C
+    restatement of select_grid -> find_edge -> heap_merge over EVERY interval
+    of the product each timed step (the whole workload, all host threads),
+    plus one timing of the reference's own Python path on a 1/64 slice."""
     rank = int(os.environ.get("RANK", "0"))
-    world = int(os.environ.get("WORLD_SIZE", "1"))
+    world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
     if rank != 0:
         return 0
+    from oracle import oracle as O
     f, g = operands(args)
     threads = cpu_threads()
-    vals = []
-    desc = ""
-    for k in range(args.warmup + args.steps):
-        v, desc, pairs, dt = cpu_sample(f, g, 4.0, threads)
-        if k >= args.warmup:
-            vals.append((pairs, dt))
-    tp = sum(p for p, _ in vals)
-    tt = sum(d for _, d in vals)
-    value = tp / tt
+    bounds = O.select_grid(f, g, 64)
+    P = f.n * g.n
+    full = os.environ.get("REF_SAMPLE_STRIDE") is None
+    stride = 1 if full else int(os.environ["REF_SAMPLE_STRIDE"])
+    pairs = P if stride == 1 else O.sample_pairs(f, g, bounds, stride)
+    # warm-up steps are untimed: a 1/64 sample each (the whole product takes
+    # ~10 s per step on 16 threads)
+    for _ in range(args.warmup):
+        O.mul_raw(f, g, threads=threads, bounds=bounds, stride=64)
+    tt = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        O.mul_raw(f, g, threads=threads, bounds=bounds, stride=stride)
+        tt.append(time.perf_counter() - t0)
+    value = pairs * len(tt) / sum(tt)
+    desc = (f"every interval of {len(bounds) - 1} select_grid(l=64) intervals ({P} term products: the whole "
+            f"product), C heap_merge port, {threads} threads" if stride == 1 else
+            f"every {stride}th of {len(bounds) - 1} intervals ({pairs} of {P} term products), C heap_merge "
+            f"port, {threads} threads")
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * tt / max(1, len(vals)),
+            "warmup": args.warmup, "ms_per_step": 1e3 * sum(tt) / max(1, len(tt)),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "int64" if args.coeff == "int" else "f64", "data": "synthetic (closed form)",
             "impl": "reference",
-            "config": {"workload": workload_name(args, f, g), "sample": desc},
+            "config": {"workload": workload_name(args, f, g), "sample": desc, "cpu_model": cpu_model()},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port",
-                             "sample": desc},
+                             "sample": desc, "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    if not os.environ.get("NO_PY_REFERENCE"):
+        try:
+            line["python_reference"] = python_reference_sample(f, g, threads)
+        except Exception as exc:  # reported, never fatal for the CPU arm
+            line["python_reference"] = {"unavailable": f"{type(exc).__name__}: {exc}"}
+        pr = line["python_reference"]
+        if pr and "value" in pr:
+            line["python_reference"]["port_speedup"] = value / pr["value"]
     print(json.dumps(line), flush=True)
     return 0
 
 
 def verify_product(args, f, step, gathered, world, rank):
     """sha256 of the reference text format of the (assembled) product vs the
-    reference's recorded digest (tests/golden/digests.json)."""
+    reference's recorded digest (tests/golden/digests.json); rank 0 only."""
     import numpy as np
     from paper_1303_7425_b200 import io
     from paper_1303_7425_b200.core import Polynomial
@@ -258,16 +316,20 @@ def verify_product(args, f, step, gathered, world, rank):
     want = json.loads((ROOT / "tests" / "golden" / "digests.json").read_text())["products"]
     key = f"{args.config}/{args.coeff}"
     r = step()
-    if world > 1:
-        e, c = gathered[0]
-        exps = e.cpu().numpy().view(np.uint64)
-        words = c.cpu().numpy().view(np.uint64)
-    else:
-        e, c = r.tensors()
-        exps = e.cpu().numpy().view(np.uint64)
-        words = c.cpu().numpy().view(np.uint64).reshape(exps.shape[0], -1)
+    exps = words = None
+    if rank == 0:
+        if world > 1:
+            e, c = gathered[0]
+            exps = e.cpu().numpy().view(np.uint64)
+            words = c.cpu().numpy().view(np.uint64)
+        else:
+            e, c = r.tensors()
+            exps = e.cpu().numpy().view(np.uint64)
+            words = c.cpu().numpy().view(np.uint64).reshape(exps.shape[0], -1)
     if r is not None:
         r.free()
+    if rank != 0:
+        return None
     if args.coeff == "float":
         co = words.reshape(-1).view(np.float64).tolist()
     else:
@@ -278,22 +340,57 @@ def verify_product(args, f, step, gathered, world, rank):
     return {"digest": got, "reference_digest": want.get(key, {}).get("sha256"), "ok": ok, "terms": p.n}
 
 
+def free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` without torchrun: launch N ranks (one process per
+    GPU) through torch.distributed.run on 127.0.0.1.  With fewer devices than
+    ranks the ranks are emulated on the available devices over gloo (a
+    correctness run: the line says so, and its times are not a scaling
+    measurement)."""
+    from paper_1303_7425_b200 import _native
+    ndev = _native.load().pgpu_device_count()
+    argv = list(sys.argv[1:])
+    if ndev < args.gpus and not args.emulate_ranks:
+        print(f"[bench] {args.gpus} ranks requested, {ndev} CUDA device(s) visible: emulating the ranks "
+              "over gloo (correctness only)", file=sys.stderr, flush=True)
+        argv.append("--emulate-ranks")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", f"--master-port={free_port()}", str(Path(__file__).resolve()), *argv]
+    env = dict(os.environ)
+    env.setdefault("OMP_NUM_THREADS", "1")
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
     import numpy as np
     import torch
     import torch.distributed as dist
-    from paper_1303_7425_b200 import MulConfig, _native
-    from paper_1303_7425_b200.cluster import plan_for_ranks, rank_range, gather_slices
+    from paper_1303_7425_b200 import _native
+    from paper_1303_7425_b200.cluster import PeerGather, gather_slices, make_plan
     from paper_1303_7425_b200.core import SENTINEL
-    from paper_1303_7425_b200.device import DeviceOperand, mul_host_pinned, mul_on_device
+    from paper_1303_7425_b200.device import (DeviceOperand, PinnedOperand, mul_host_pinned,
+                                             mul_on_device)
     from paper_1303_7425_b200.parmul import Operand, count_below
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = 0 if args.emulate_ranks else int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = _native.load().pgpu_device_count()
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.emulate_ranks:
+        local = local % max(1, ndev)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
@@ -301,7 +398,6 @@ def main():
             dist.init_process_group("gloo")
         else:
             dist.init_process_group("nccl", device_id=dev)
-    _native.load()
 
     f, g = operands(args)
     A, B = Operand.from_poly(f), Operand.from_poly(g)
@@ -312,43 +408,49 @@ def main():
     # partition (paper Alg. 2): planned once per operand pair, timed separately
     t0 = time.perf_counter()
     lo, hi = 0, SENTINEL
+    plan = None
     if world > 1:
-        bounds, plan = plan_for_ranks(f, g, 64, world, rank,
-                                      lambda x, y, b: count_below(x, y, b, device=local), None)
-        lo, hi = rank_range(bounds, plan, rank)
+        plan = make_plan(f, g, 64, world, rank, lambda x, y, b: count_below(x, y, b, device=local))
+        lo, hi = plan.range_of(rank)
     plan_ms = 1e3 * (time.perf_counter() - t0)
+    my_pairs = [0]  # this range's pair count, reported by the first product (the plan's cache)
 
     total_pairs = f.n * g.n
-
-    def step(timing=False):
-        if lo >= hi:
-            res = None
-        else:
-            res = mul_on_device(dA, dB, f.layout, lo=lo, hi=hi, path=args.path, device=local,
-                                stream=sptr, timing=timing)
-        if world > 1:
-            if res is not None:
-                e, c = res.tensors()
-                c = c.view(torch.int64).reshape(e.shape[0], -1)
-            else:
-                e = torch.zeros(0, dtype=torch.int64, device=dev)
-                c = torch.zeros((0, 3), dtype=torch.int64, device=dev)
-            if peer[0] is not None:
-                gathered[0] = peer[0].gather(e, c, stream=sptr)
-            else:
-                gathered[0] = gather_slices(e, c)
-        return res
-
     gathered = [None]
-    # final gather of disjoint slices: peer copies over NVLink (CUDA IPC), or
-    # NCCL / gloo all-gather with --gather collective
-    peer = [None]
     gather_kind = "none"
+    peer = None
     if world > 1:
         gather_kind = args.gather
         if args.gather == "peer":
-            from paper_1303_7425_b200.cluster import PeerGather
-            peer[0] = PeerGather(device=local)
+            peer = PeerGather(device=local, dst=0)
+
+    def range_product(Ain, Bin, timing=False, inputs_on_device=True):
+        if lo >= hi:
+            return None
+        r = mul_on_device(Ain, Bin, f.layout, lo=lo, hi=hi, path=args.path, device=local, stream=sptr,
+                          timing=timing, range_pairs=my_pairs[0], inputs_on_device=inputs_on_device)
+        my_pairs[0] = r.pairs
+        return r
+
+    def gather(res):
+        if res is not None:
+            e, c = res.tensors()
+            c = c.view(torch.int64).reshape(e.shape[0], -1)
+        else:
+            e = torch.zeros(0, dtype=torch.int64, device=dev)
+            c = torch.zeros((0, 3 if args.coeff == "int" else 1), dtype=torch.int64, device=dev)
+        if peer is not None:
+            gathered[0] = peer.gather(e, c, stream=sptr)
+        else:
+            gathered[0] = gather_slices(e, c)
+
+    def step(timing=False, ev=None):
+        res = range_product(dA, dB, timing=timing)
+        if world > 1:
+            if ev is not None:
+                ev.record(stream)
+            gather(res)
+        return res
 
     flush = torch.empty(args.flush_mib * (1 << 20) // 4, dtype=torch.float32, device=dev)
     for _ in range(args.warmup):
@@ -363,19 +465,22 @@ def main():
     torch.cuda.synchronize()
     if clocks is not None:
         clocks.start()
-    times = []
+    times, prod_ms = [], []
     launches = 0
     last = None
     for _ in range(args.steps):
         if not args.no_flush:
             flush.zero_()  # evict L2 between timed steps
         e0 = torch.cuda.Event(enable_timing=True)
+        em = torch.cuda.Event(enable_timing=True)
         e1 = torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        r = step()
+        r = step(ev=em)
         e1.record(stream)
         e1.synchronize()
         times.append(e0.elapsed_time(e1))
+        if world > 1:
+            prod_ms.append(e0.elapsed_time(em))
         if r is not None:  # same allocation pattern as the warm-up: free before the next step
             launches += r.launches
             last = (r.n, r.nl, r.path)
@@ -387,6 +492,8 @@ def main():
     my_ms = sum(times)
     t = torch.tensor([my_ms], dtype=torch.float64, device=dev)
     if world > 1:
+        if args.emulate_ranks:
+            t = t.cpu()
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     total_ms = float(t.item())
     ms_per_step = total_ms / args.steps
@@ -406,7 +513,20 @@ def main():
         for k, v in pr.items():
             phases.setdefault(k, []).append(v)
     phases = {k: statistics.median(v) for k, v in phases.items()}
-    my_pairs = total_pairs if world == 1 else None
+    multi = None
+    if world > 1:
+        # per step: range product vs gather + synchronisation (max over ranks)
+        mine = [statistics.median(prod_ms), statistics.median([a - b for a, b in zip(times, prod_ms)])]
+        tt = torch.tensor(mine, dtype=torch.float64, device=dev)
+        if args.emulate_ranks:
+            tt = tt.cpu()
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        nterms = torch.tensor([float(n_out)], dtype=torch.float64, device=dev)
+        nterms = nterms.cpu() if args.emulate_ranks else nterms
+        dist.all_reduce(nterms)
+        multi = {"product_ms": float(tt[0]), "gather_ms": float(tt[1]),
+                 "non_product_ms": ms_per_step - float(tt[0]), "terms": int(nterms.item())}
+        phases["gather"] = float(tt[1])
 
     out = None
     if rank == 0:
@@ -416,9 +536,10 @@ def main():
         cands = {k: phases[k] for k in ("numeric", "sort", "reduce", "bucket_reduce") if k in phases}
         kern = max(cands, key=cands.get) if cands else None
         kern_ms = phases.get(kern, float("nan")) if kern else float("nan")
+        n_all = multi["terms"] if multi else n_out
         w_c = 8 if args.coeff == "float" else 8 * nl
         w_in = 8 if A.kind != 2 else 16
-        b_alg_step = 32 * total_pairs + (8 + w_c) * n_out + (8 + w_in) * (f.n + g.n)
+        b_alg_step = 32 * total_pairs + (8 + w_c) * n_all + (8 + w_in) * (f.n + g.n)
         kern_pairs = total_pairs / world
         achieved = 32 * kern_pairs / (kern_ms / 1e3) / 1e9 if kern else None
         traffic = None
@@ -440,65 +561,123 @@ def main():
                                      "so frac > 1 means it moves less than the modelled pipeline",
                 "step_frac": b_alg_step / (ms_per_step / 1e3) / 1e9 / (peak * world),
                 "phases_ms": phases}
+        emulated = bool(args.emulate_ranks and world > 1)
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "int64" if args.coeff == "int" else "f64",
                "data": "synthetic (closed-form Fateman/Monagan-Pearce operands)",
                "config": {"workload": workload_name(args, f, g), "term_products": total_pairs,
-                          "result_terms": n_out, "path": path_used, "result_limbs": nl,
+                          "result_terms": n_all, "path": path_used, "result_limbs": nl,
                           "arithmetic": ("exact integers: int64 operands, 128-bit products, "
                                          "accumulators proven wide enough (Fateman n=30: 136-bit)")
                           if args.coeff == "int" else "f64",
-                          "parallelism": f"partition_by_ops x{world}" if world > 1 else "1 GPU",
-                          "gather": {"peer": "peer copies of disjoint slices (CUDA IPC, NVLink)",
+                          "parallelism": (f"partition_by_ops x{world}" +
+                                          (f", ranks emulated on {max(1, ndev)} device(s) over gloo "
+                                           "(correctness run; times are not a scaling measurement)"
+                                           if emulated else "")) if world > 1 else "1 GPU",
+                          "gather": {"peer": "peer copies of disjoint slices to rank 0 (CUDA IPC, "
+                                             "NVLink); counts and completion stream-ordered over NCCL",
                                      "collective": "all-gather of disjoint slices",
                                      "none": "none (1 GPU)"}[gather_kind],
                           "l2": f"flushed ({args.flush_mib} MiB write) between timed steps",
+                          "plan": "select_grid(l=64) + O_k partition (partition_by_ops), and each "
+                                  "range's pair count from the first product: once per operand pair"
+                          if world > 1 else "none (1 GPU)",
                           "plan_ms": plan_ms, "step_ms": [round(x, 3) for x in times]},
                "roofline": roof, "gpu_launches": launches, "clocks": ck}
+        if multi:
+            out["multi_gpu"] = multi
+        if emulated:
+            out["emulated_ranks"] = True
 
-    # e2e through the C ABI with pinned host buffers (N=1 only)
-    if world == 1 and not args.no_e2e:
-        pa_e = torch.from_numpy(A.exps.view(np.int64)).pin_memory()
-        pa_c = torch.from_numpy(np.ascontiguousarray(A.coef).view(np.int64).reshape(-1)).pin_memory()
-        pb_e = torch.from_numpy(B.exps.view(np.int64)).pin_memory()
-        pb_c = torch.from_numpy(np.ascontiguousarray(B.coef).view(np.int64).reshape(-1)).pin_memory()
-        h2d = (pa_e.numel() + pa_c.numel() + pb_e.numel() + pb_c.numel()) * 8
-        e2e_t = []
-        d2h = 0
-        for k in range(args.warmup + args.steps):
-            flush.zero_()
-            torch.cuda.synchronize()
-            t1 = time.perf_counter()
-            res = mul_host_pinned(pa_e.data_ptr(), pa_c.data_ptr(), pb_e.data_ptr(), pb_c.data_ptr(),
-                                  A.n, B.n, A.kind, f.layout, path=args.path, device=local,
-                                  stream=sptr)
-            t2 = time.perf_counter()
-            d2h = int(res.n) * 8 * (1 + (int(res.acc_limbs) or 1))
-            _native.load().pgpu_free_result(__import__("ctypes").byref(res))
-            if k >= args.warmup:
-                e2e_t.append(t2 - t1)
+    # e2e through the public API with host buffers (H2D of the operands and
+    # D2H of the assembled product inside the timed region)
+    if not args.no_e2e:
+        if world == 1:
+            pa_e = torch.from_numpy(A.exps.view(np.int64)).pin_memory()
+            pa_c = torch.from_numpy(np.ascontiguousarray(A.coef).view(np.int64).reshape(-1)).pin_memory()
+            pb_e = torch.from_numpy(B.exps.view(np.int64)).pin_memory()
+            pb_c = torch.from_numpy(np.ascontiguousarray(B.coef).view(np.int64).reshape(-1)).pin_memory()
+            h2d = (pa_e.numel() + pa_c.numel() + pb_e.numel() + pb_c.numel()) * 8
+            e2e_t = []
+            d2h = 0
+            for k in range(args.warmup + args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                t1 = time.perf_counter()
+                res = mul_host_pinned(pa_e.data_ptr(), pa_c.data_ptr(), pb_e.data_ptr(), pb_c.data_ptr(),
+                                      A.n, B.n, A.kind, f.layout, path=args.path, device=local,
+                                      stream=sptr)
+                t2 = time.perf_counter()
+                d2h = int(res.n) * 8 * (1 + (int(res.acc_limbs) or 1))
+                _native.load().pgpu_free_result(__import__("ctypes").byref(res))
+                if k >= args.warmup:
+                    e2e_t.append(t2 - t1)
+            e2e_s = sum(e2e_t) / len(e2e_t)
+        else:
+            # each rank: pinned operands in, its range product, peer gather to
+            # rank 0; rank 0 copies the assembled product to pinned host memory
+            pA, pB = PinnedOperand(A), PinnedOperand(B)
+            h2d = pA.bytes + pB.bytes
+            host_out = [None]
+            e2e_t = []
+            d2h = 0
+            for k in range(args.warmup + args.steps):
+                flush.zero_()
+                torch.cuda.synchronize()
+                dist.barrier()
+                t1 = time.perf_counter()
+                r = range_product(pA, pB, inputs_on_device=False)
+                gather(r)
+                if rank == 0 and gathered[0] is not None:
+                    ge, gc = gathered[0]
+                    if host_out[0] is None or host_out[0][0].shape != ge.shape or host_out[0][1].shape != gc.shape:
+                        host_out[0] = (torch.empty(ge.shape, dtype=ge.dtype, pin_memory=True),
+                                       torch.empty(gc.shape, dtype=gc.dtype, pin_memory=True))
+                    host_out[0][0].copy_(ge, non_blocking=True)
+                    host_out[0][1].copy_(gc, non_blocking=True)
+                    d2h = (ge.numel() + gc.numel()) * 8
+                torch.cuda.synchronize()
+                t2 = time.perf_counter()
+                if r is not None:
+                    r.free()
+                if k >= args.warmup:
+                    e2e_t.append(t2 - t1)
+            mine = torch.tensor([sum(e2e_t) / len(e2e_t)], dtype=torch.float64, device=dev)
+            mine = mine.cpu() if args.emulate_ranks else mine
+            dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+            e2e_s = float(mine.item())
         if out is not None:
-            out["e2e"] = {"value": total_pairs * len(e2e_t) / sum(e2e_t), "unit": UNIT,
-                          "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                          "ms_per_step": 1e3 * sum(e2e_t) / len(e2e_t)}
+            out["e2e"] = {"value": total_pairs / e2e_s, "unit": UNIT,
+                          "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h,
+                          "ms_per_step": 1e3 * e2e_s}
     if args.verify:
         out_v = verify_product(args, f, step, gathered, world, rank)
         if out is not None:
             out["verified"] = out_v
-    if out is not None and world == 1 and not args.no_cpu_baseline:
+    if out is not None and not args.no_cpu_baseline:
         v, desc, pairs, dt = cpu_sample(f, g, 15.0, cpu_threads())
         out["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": cpu_threads(), "kind": "port",
-                               "sample": desc, "seconds": dt}
+                               "sample": desc, "seconds": dt, "cpu_model": cpu_model()}
     if out is not None:
         print(json.dumps(out), flush=True)
-    if peer[0] is not None:
-        peer[0].release()
     if world > 1:
+        if peer is not None:
+            peer.release()
         dist.barrier()
         dist.destroy_process_group()
     return 0
+
+
+def cpu_model() -> str:
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
 
 
 if __name__ == "__main__":

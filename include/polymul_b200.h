@@ -48,7 +48,7 @@ extern "C" {
 #endif
 
 #define PGPU_MAX_FIELDS 15
-#define PGPU_ABI_VERSION 2
+#define PGPU_ABI_VERSION 3
 
 typedef enum pgpu_status {
   PGPU_OK = 0,
@@ -116,6 +116,10 @@ typedef struct pgpu_options {
   uint64_t hi;                      /*   satisfies lo <= s < hi (hi = 2^64-1:   */
                                     /*   no upper limit).  split= / cluster range */
   void* stream;                     /* cudaStream_t to run on, NULL = library's */
+  int64_t range_pairs;              /* 0, or the pair count of [lo, hi) for these
+                                       operands (pgpu_result.pairs of an earlier
+                                       call with the same operands and range: a
+                                       cluster plan); skips the device count    */
 } pgpu_options;
 
 #define PGPU_NPHASE 8

@@ -26,6 +26,7 @@ EXPORTS = ("pgpu_default_options", "pgpu_mul", "pgpu_count_below", "pgpu_free_re
            "pgpu_ipc_free", "pgpu_copy", "pgpu_stream_sync", "pgpu_last_error", "pgpu_device_count",
            "pgpu_abi_version")
 IPC_HANDLE_BYTES = 64
+ABI_VERSION = 3  # PGPU_ABI_VERSION of include/polymul_b200.h (the ctypes structs below)
 
 
 class Layout(C.Structure):
@@ -41,7 +42,8 @@ class Options(C.Structure):
     _fields_ = [("coef_kind", C.c_int32), ("acc_limbs", C.c_int32), ("device", C.c_int32),
                 ("path", C.c_int32), ("float_ordered", C.c_int32), ("timing", C.c_int32),
                 ("inputs_on_device", C.c_int32), ("outputs_on_device", C.c_int32),
-                ("lo", C.c_uint64), ("hi", C.c_uint64), ("stream", C.c_void_p)]
+                ("lo", C.c_uint64), ("hi", C.c_uint64), ("stream", C.c_void_p),
+                ("range_pairs", C.c_int64)]
 
 
 class Result(C.Structure):
@@ -109,6 +111,9 @@ def load(path: Path | None = None) -> C.CDLL:
         lib.pgpu_device_count.restype = C.c_int
         lib.pgpu_abi_version.argtypes = []
         lib.pgpu_abi_version.restype = C.c_int
+        if lib.pgpu_abi_version() != ABI_VERSION:
+            raise NativeError(f"{p}: ABI version {lib.pgpu_abi_version()}, expected {ABI_VERSION} "
+                              "(stale build: run python -m paper_1303_7425_b200.build)")
         _lib = lib
         return lib
 

@@ -100,6 +100,43 @@ def plan_for_ranks(a, b, l: int, world: int, rank: int, count_fn, group=None):
     return bounds, partition_by_ops(op_counts, world)
 
 
+@dataclass
+class RankPlan:
+    """Paper Alg. 2 for one operand pair, planned once (it depends only on the
+    operands' supports, like an FFT plan): the bounds, the partition, every
+    rank's packed range, and each range's pair count once known (the library
+    reports it with the first product; later products pass it back as
+    `range_pairs` and skip the device count)."""
+    bounds: list
+    plan: ClusterPlan
+    ranges: list
+    pairs: list
+
+    @property
+    def n(self) -> int:
+        return self.plan.n_nodes
+
+    def range_of(self, rank: int) -> tuple:
+        return self.ranges[rank]
+
+
+def make_plan(a, b, l: int, world: int, rank: int, count_fn, group=None) -> RankPlan:
+    """Each rank counts O_k for its block of intervals; counts all-gathered."""
+    bounds, plan = plan_for_ranks(a, b, l, world, rank, count_fn, group)
+    return RankPlan(bounds, plan, [rank_range(bounds, plan, r) for r in range(world)], [0] * world)
+
+
+def plan_all_ranks(a, b, l: int, n: int, count_fn) -> RankPlan:
+    """The N-rank plan computed by one process (every block's O_k on this
+    GPU): the virtual-rank mode, where one GPU runs the N range products one
+    after another (partition parity at N = 8 on a single device)."""
+    bounds = select_grid(a, b, GridParams(l)).bounds
+    cum = count_fn(a, b, bounds)
+    op_counts = [int(cum[k + 1] - cum[k]) for k in range(len(bounds) - 1)]
+    plan = partition_by_ops(op_counts, n)
+    return RankPlan(bounds, plan, [rank_range(bounds, plan, r) for r in range(n)], [0] * n)
+
+
 def gather_slices(exps, coef, group=None, device=None):
     """All-gather disjoint ordered slices (torch tensors) into rank order.
 
@@ -142,38 +179,57 @@ def gather_slices(exps, coef, group=None, device=None):
 
 class PeerGather:
     """The final step of paper Alg. 2 as peer copies over NVLink (the north
-    star's "peer copies, no reduction collective"): every rank holds the
-    assembled product in a CUDA-IPC-shareable buffer whose handle the other
-    ranks open once; each rank then copies its own ordered slice straight into
-    every rank's buffer at its offset (device-to-device, through the peer
-    mapping), and a barrier marks all slices in place.  Buffers and peer
-    mappings are reused while the assembled size stays the same."""
+    star's "peer copies, no reduction collective").  The destination rank(s)
+    hold the assembled product in a CUDA-IPC-shareable buffer whose handle the
+    other ranks open once; each rank copies its own ordered slice straight
+    into the destination buffer at its offset (device to device, through the
+    peer mapping).  dst = r: only rank r assembles (N-1 copies, the
+    reference's gather to node 0, cluster.py:311-317); dst = None: every rank
+    does (an all-gather).
 
-    def __init__(self, group=None, device: int = 0):
+    Per step under NCCL the synchronisation is stream-ordered: the term counts
+    are one all-gather of an int64, and completion is an all-reduce of one
+    word enqueued after the copies (each rank's copies precede it on its
+    stream), so no host barrier and no pickled object exchange.  Buffers and
+    peer mappings are reused while the assembled size stays the same."""
+
+    def __init__(self, group=None, device: int = 0, dst: int | None = None):
+        import torch
+        import torch.distributed as dist
         from . import _native as N
         self.N, self.lib = N, N.load()
-        self.group, self.device = group, device
+        self.group, self.device, self.dst_rank = group, device, dst
+        self.nccl = dist.get_backend(group) == "nccl"
         self.shape = None
         self.bufs, self.dst = [], []
+        dev = torch.device("cuda", device)
+        self.cnt = torch.zeros(1, dtype=torch.int64, device=dev)
+        self.cnts = torch.zeros(dist.get_world_size(group), dtype=torch.int64, device=dev)
+        self.tick = torch.zeros(1, dtype=torch.int32, device=dev)
 
     def _check(self, st):
         if st != self.N.PGPU_OK:
             raise self.N.NativeError(self.N.last_error())
+
+    def _dests(self, world):
+        return list(range(world)) if self.dst_rank is None else [self.dst_rank]
 
     def _setup(self, total: int, w: int):
         import ctypes as C
         import torch.distributed as dist
         self.release()
         rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
-        handles = []
-        for nbytes in (total * 8, total * w * 8):
-            ptr, h = C.c_void_p(), C.create_string_buffer(self.N.IPC_HANDLE_BYTES)
-            self._check(self.lib.pgpu_ipc_alloc(nbytes, self.device, C.byref(ptr), h))
-            self.bufs.append(ptr.value)
-            handles.append(h.raw)
-        peers = _allgather_obj(handles, self.group)
+        handles = None
+        if rank in self._dests(world):
+            handles = []
+            for nbytes in (total * 8, total * w * 8):
+                ptr, h = C.c_void_p(), C.create_string_buffer(self.N.IPC_HANDLE_BYTES)
+                self._check(self.lib.pgpu_ipc_alloc(nbytes, self.device, C.byref(ptr), h))
+                self.bufs.append(ptr.value)
+                handles.append(h.raw)
+        peers = _allgather_obj(handles, self.group)  # once per assembled shape
         self.dst = []
-        for r in range(world):
+        for r in self._dests(world):
             if r == rank:
                 self.dst.append((self.bufs[0], self.bufs[1], False))
                 continue
@@ -185,14 +241,23 @@ class PeerGather:
             self.dst.append((opened[0], opened[1], True))
         self.shape = (total, w)
 
+    def counts(self, n: int) -> list:
+        import torch.distributed as dist
+        if self.nccl:
+            self.cnt.fill_(n)
+            dist.all_gather_into_tensor(self.cnts, self.cnt, group=self.group)
+            return [int(x) for x in self.cnts.tolist()]
+        return [int(x) for x in _allgather_obj(n, self.group)]
+
     def gather(self, exps, coef, stream=None):
-        """(exps int64[total], coef int64[total, w]) views of the assembled product."""
+        """(exps int64[total], coef int64[total, w]) views of the assembled
+        product on a destination rank; None on the others."""
         import torch
         import torch.distributed as dist
         from .device import _CudaArray
-        rank = dist.get_rank(self.group)
+        rank, world = dist.get_rank(self.group), dist.get_world_size(self.group)
         n, w = int(exps.shape[0]), int(coef.shape[1])
-        counts = [int(x) for x in _allgather_obj(n, self.group)]
+        counts = self.counts(n)
         off = sum(counts[:rank])
         total = sum(counts)
         if self.shape != (total, w):
@@ -201,8 +266,13 @@ class PeerGather:
         for de, dc, _ in self.dst:
             self._check(self.lib.pgpu_copy(de + off * 8, exps.data_ptr(), n * 8, self.device, st))
             self._check(self.lib.pgpu_copy(dc + off * w * 8, coef.data_ptr(), n * w * 8, self.device, st))
-        self._check(self.lib.pgpu_stream_sync(self.device, st))
-        dist.barrier(self.group)  # every rank's slice is in every buffer
+        if self.nccl:
+            dist.all_reduce(self.tick, group=self.group)  # stream-ordered: all slices in place
+        else:  # gloo (rank emulation): host-side completion
+            self._check(self.lib.pgpu_stream_sync(self.device, st))
+            dist.barrier(self.group)
+        if rank not in self._dests(world):
+            return None
         dev = torch.device("cuda", self.device)
         if total == 0:
             return torch.zeros(0, dtype=torch.int64, device=dev), torch.zeros((0, w), dtype=torch.int64, device=dev)
@@ -212,7 +282,7 @@ class PeerGather:
     def release(self):
         """Unmap the peers' buffers and free ours (collective: call on every rank)."""
         import torch.distributed as dist
-        if not self.bufs:
+        if self.shape is None:
             return
         dist.barrier(self.group)  # nobody still writes into our buffers
         for de, dc, opened in self.dst:

@@ -17,20 +17,19 @@
 //   B3 k_bin_scatter  the same walk writes (key - KL, i<<32|j) once, at
 //                     offset(bin) + atomic run position: records of one bucket
 //                     are contiguous
-//   B4 k_bucket_reduce one CTA per bucket: coalesced record loads and
-//                     coefficient products; keys hashed into a shared-memory
-//                     table whose slots accumulate the exact sums (32-bit
-//                     atomics with explicit carries; f64 atomics in fast
-//                     mode); distinct keys ranked (counting rank, or bitonic
-//                     above 256); nonzero terms (merge.py:63) appended to a
-//                     staging run.  A bucket that is one large bin is reduced
-//                     in dense mode over the bin's key window.
-//   B5 k_bucket_gather bucket runs -> final positions (bucket order = key
-//                     order), one warp per bucket
+//   B4 k_bucket_reduce persistent CTAs claim buckets in key order: keys
+//                     grouped in a shared-memory table (CAS on keys only),
+//                     distinct keys ranked, records placed in (key, row)
+//                     order, products folded by one owner per key in that
+//                     order (no atomics on coefficient data: integers exact,
+//                     doubles in the reference's order and run-to-run
+//                     identical), zero sums dropped (merge.py:63); a decoupled
+//                     look-back over the buckets' term counts places the terms
+//                     at their final positions.  A bin above the bucket bound
+//                     sends the batch to the sort path.
 //
 // DRAM traffic per pair: one record write + one record read (12-16 B each),
-// against 5-6 read+write passes on the sort path.  The float-ordered mode
-// (reference summation order) stays on the sort path.
+// against 5-6 read+write passes on the sort path.
 #pragma once
 #include "common.cuh"
 #include "scan.cuh"
@@ -38,11 +37,10 @@
 namespace pgpu {
 
 #ifndef PGPU_BUCKET_CAP
-#define PGPU_BUCKET_CAP 512
+#define PGPU_BUCKET_CAP 2048
 #endif
 constexpr int kBucketCap = PGPU_BUCKET_CAP;  // pairs per bucket (max)
 constexpr int kBucketHalf = kBucketCap / 2;
-constexpr int kBucketTable = 2 * kBucketCap; // hash slots (load factor <= 1/2)
 #ifndef PGPU_BUCKET_THREADS
 #define PGPU_BUCKET_THREADS 256
 #endif
@@ -179,35 +177,64 @@ struct BStartOut {
 };
 
 // ---- B4 ---------------------------------------------------------------------
+// Persistent CTAs claim buckets in key order.  A bucket's records are grouped
+// by key without touching coefficient data atomically:
+//   1. keys -> open-addressing slots (CAS on the key only; equal keys share a slot)
+//   2. distinct keys compacted; their count is published at once for a
+//      decoupled look-back over the buckets (warp 0 resolves the bucket's
+//      output base while the other warps rank the keys)
+//   3. the distinct keys are ranked (counting rank, or a bitonic sort above 224)
+//   4. per key rank: record count (the returned index is an arbitrary position
+//      in the key's run), exclusive scan -> run starts; each record's position
+//      in (key, row) order: floats rank their row among the run's rows (the
+//      reference's tie order, merge.py:32-33), integers keep the arbitrary
+//      position (exact sums do not depend on the order)
+//   5. each record's product is written at its position; one owner per key
+//      folds its run in order (acc = p_first; acc += p ...; merge.py:49-58)
+//   6. term r of the bucket goes to base + r (bucket order = key order): no
+//      staging and no gather pass.  A zero sum (merge.py:63) leaves its slot
+//      marked with the all-ones exponent (SENTINEL, never a term) and is
+//      counted; the driver compacts only if any occurred.
+constexpr int kBkIpt = kBucketCap / kBucketThreads;  // records per thread
+constexpr int kBkTable = 2 * kBucketCap;             // hash slots (load factor <= 1/2)
+constexpr int kBkSlotBits = 12;
+static_assert(kBkTable <= (1 << kBkSlotBits), "slot index must fit the sort word");
+constexpr unsigned long long kBkAgg = 1ull << 62;    // look-back flags (value in the low 62 bits)
+constexpr unsigned long long kBkPre = 2ull << 62;
+constexpr unsigned long long kBkVal = (1ull << 62) - 1;
+constexpr uint32_t kBkRankThreads = kBucketThreads - 32;  // warp 0 runs the look-back meanwhile
+
 struct BucketArgs {
   const void* rkey;            // KT keys relative to KL
   const uint64_t* rid;         // i<<32 | j
   const uint32_t* binoff;      // nbins offsets
   const uint32_t* bstart;      // nbuckets+1 first bins
-  uint32_t nbins, pairs;
-  int s1;                      // bin map (dense-mode key window)
-  const uint32_t* tab;
+  uint32_t nbins, pairs, nbuckets;
   const void* ac;
   const void* bc;
   uint64_t KL;
   KeyPlan P;
-  uint64_t* sexp;              // staging terms (capacity scap)
-  uint64_t* scoef;
-  uint64_t scap;
-  unsigned long long* sctr;    // staging bump counter
-  uint64_t* bbase;             // per bucket: staging base
-  uint32_t* bnnz;              // per bucket: nonzero terms
-  uint32_t* overflow;
+  uint64_t* oexp;              // distinct keys in key order (capacity: pairs)
+  uint64_t* ocoef;             // NL limbs per term (f64: the double's bits)
+  unsigned long long* status;  // [nbuckets] look-back words (zeroed)
+  unsigned int* ticket;        // next bucket to claim (zeroed)
+  uint32_t* overflow;          // a bucket above kBucketCap records: the batch takes the sort path
+  unsigned long long* zeros;   // zero sums written as holes
 };
 
-template <typename KT, int NL>
+template <typename KT, int NL, bool ROWS>
 struct BucketSmem {
-  uint32_t acc[kBucketTable][2 * NL]; // per hash slot (dense mode: per key): the sum
-  KT hkey[kBucketTable];              // open-addressing key table
-  uint64_t sortv[kBucketCap];         // key << 12 | slot, sorted by key
-  uint32_t scan[kBucketTable];        // occupied-slot flags, then nonzero-term flags
+  KT hkey[kBkTable];                 // open-addressing key table
+  uint16_t rank[kBkTable];           // key rank of an occupied slot
+  union {
+    uint64_t sortv[kBucketCap];      // distinct keys: key << 12 | slot
+    uint64_t prod[kBucketCap * NL];  // products at their (key, row) positions; then run sums
+  };
+  KT keyr[kBucketCap];               // key of each rank
+  uint32_t start[kBucketCap + 1];    // per key rank: count, then run start
+  uint32_t rows[ROWS ? kBucketCap : 1];  // rows at arbitrary run positions (f64 tie order)
   uint32_t sh[33];
-  uint32_t ndist;
+  uint32_t bucket;
   unsigned long long base;
 };
 
@@ -220,28 +247,7 @@ __device__ __forceinline__ uint64_t cas_key(uint64_t* p, uint64_t cmp, uint64_t 
 }
 
 __device__ __forceinline__ uint32_t bucket_hash(uint64_t k) {
-  return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> 40) & (kBucketTable - 1);
-}
-
-// Exact accumulation of an NL-limb two's-complement product into 2*NL 32-bit
-// words with native shared-memory atomics: the carry out of each word is
-// recovered from the returned old value and added into the next word, so the
-// words hold the exact sum modulo 2^(64 NL) whatever the interleaving.
-template <int NL>
-__device__ __forceinline__ void acc_add(uint32_t* a, const Limbs<NL>& p) {
-  uint32_t carry = 0;
-#pragma unroll
-  for (int w = 0; w < 2 * NL; ++w) {
-    const uint32_t pw = (uint32_t)(p.w[w >> 1] >> (32 * (w & 1)));
-    const uint32_t x = pw + carry;
-    const uint32_t c1 = x < pw ? 1u : 0u;
-    if (x == 0u) {
-      carry = c1;
-      continue;
-    }
-    const uint32_t old = atomicAdd(a + w, x);
-    carry = c1 + ((uint32_t)(old + x) < old ? 1u : 0u);
-  }
+  return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> 40) & (kBkTable - 1);
 }
 
 // exclusive scan of x[0, n) in place, C items per thread (n <= C * blockDim),
@@ -266,221 +272,380 @@ __device__ __forceinline__ uint32_t chunk_scan(uint32_t* x, uint32_t n, uint32_t
   return tot;
 }
 
-template <int NL, int CK>
-__device__ __forceinline__ void add_product(const BucketArgs& A, uint32_t* acc, uint64_t id) {
-  const uint64_t i = id >> 32, j = id & 0xffffffffu;
-  if constexpr (CK == 0) {
-    const double pr = __dmul_rn(__ldg(reinterpret_cast<const double*>(A.ac) + i),
-                                __ldg(reinterpret_cast<const double*>(A.bc) + j));
-    atomicAdd(reinterpret_cast<double*>(acc), pr);
-  } else {
-    acc_add<NL>(acc, imul<NL, CK>(load_icoef<CK>(A.ac, (int64_t)i), load_icoef<CK>(A.bc, (int64_t)j)));
-  }
+// ---- block bitonic sort of 256*E words held blocked (thread t: [t*E, t*E+E)) --
+__device__ __forceinline__ void bitonic_keep(uint64_t& a, uint64_t o, uint32_t x, uint32_t s, uint32_t k) {
+  const bool up = (x & k) == 0, lower = (x & s) == 0;
+  const uint64_t lo = a < o ? a : o, hi = a < o ? o : a;
+  a = (lower == up) ? lo : hi;
 }
 
-template <int NL, int CK>
-__device__ __forceinline__ bool acc_nonzero(const uint32_t* acc) {
-  if constexpr (CK == 0) {
-    return __longlong_as_double((long long)(((uint64_t)acc[1] << 32) | acc[0])) != 0.0;  // NaN kept
-  } else {
-    uint32_t o = 0;
+template <int E, int S>
+__device__ __forceinline__ void bitonic_reg(uint64_t (&v)[E], uint32_t t, uint32_t k) {
 #pragma unroll
-    for (int w = 0; w < 2 * NL; ++w) o |= acc[w];
-    return o != 0;
-  }
-}
-
-// Staging: one bump-allocated run per bucket; returns the run base, or ~0 on overflow
-__device__ __forceinline__ unsigned long long bucket_alloc(const BucketArgs& A, uint32_t k,
-                                                           uint32_t nnz, unsigned long long* sbase) {
-  if (threadIdx.x == 0) {
-    unsigned long long b = atomicAdd(A.sctr, (unsigned long long)nnz);
-    if (b + nnz > A.scap) {
-      *A.overflow = 1u;
-      b = ~0ull;
-    }
-    *sbase = b;
-    A.bbase[k] = b;
-    A.bnnz[k] = nnz;
-  }
-  __syncthreads();
-  return *sbase;
-}
-
-template <int NL>
-__device__ __forceinline__ void write_term(const BucketArgs& A, uint64_t pos, uint64_t key,
-                                           const uint32_t* acc) {
-  A.sexp[pos] = expand_key(A.KL + key, A.P);
-#pragma unroll
-  for (int w = 0; w < NL; ++w)
-    A.scoef[pos * NL + w] = ((uint64_t)acc[2 * w + 1] << 32) | acc[2 * w];
-}
-
-// Dense mode for a bucket that is one fine bin above the record bound (many
-// pairs on few keys): accumulators indexed by key - window base.  The window
-// is the bin's key range (2^(s1 - r) keys); one wider than the table sets the
-// overflow flag and the batch takes the sort path.
-template <typename KT, int NL, int CK>
-__device__ void bucket_dense(const BucketArgs& A, BucketSmem<KT, NL>& S, uint32_t k,
-                             const KT* __restrict__ rkey, const uint64_t* __restrict__ rid,
-                             uint32_t n) {
-  const uint64_t key0 = (uint64_t)rkey[0];
-  const uint32_t t = A.tab[key0 >> A.s1];
-  const int sh = A.s1 - (int)(t & 31u);
-  const uint64_t wbase = (key0 >> sh) << sh;
-  if (sh > 20 || (1u << sh) > (uint32_t)kBucketTable) {
-    if (threadIdx.x == 0) {
-      *A.overflow = 1u;
-      A.bnnz[k] = 0;
-    }
-    return;
-  }
-  const uint32_t span = 1u << sh;
-  for (uint32_t x = threadIdx.x; x < span * 2 * NL; x += blockDim.x) (&S.acc[0][0])[x] = 0;
-  __syncthreads();
-  for (uint32_t q = threadIdx.x; q < n; q += blockDim.x)
-    add_product<NL, CK>(A, S.acc[(uint64_t)rkey[q] - wbase], rid[q]);
-  __syncthreads();
-  for (uint32_t x = threadIdx.x; x < span; x += blockDim.x) S.scan[x] = acc_nonzero<NL, CK>(S.acc[x]);
-  __syncthreads();
-  const uint32_t nnz = chunk_scan<kBucketTable / kBucketThreads>(S.scan, span, S.sh);
-  const unsigned long long base = bucket_alloc(A, k, nnz, &S.base);
-  if (base == ~0ull) return;
-  for (uint32_t x = threadIdx.x; x < span; x += blockDim.x) {
-    const uint32_t nxt = x + 1 < span ? S.scan[x + 1] : nnz;
-    if (nxt != S.scan[x]) write_term<NL>(A, base + S.scan[x], wbase + x, S.acc[x]);
-  }
-}
-
-// CK: 0 f64 (fast mode, NL = 1), 1 int64, 2 int128 operands; NL result limbs
-template <typename KT, int NL, int CK>
-__global__ void __launch_bounds__(kBucketThreads)
-k_bucket_reduce(BucketArgs A) {
-  constexpr int IPT = kBucketCap / kBucketThreads;
-  constexpr int TPT = kBucketTable / kBucketThreads;
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  BucketSmem<KT, NL>& S = *reinterpret_cast<BucketSmem<KT, NL>*>(smem_raw);
-  const uint32_t k = blockIdx.x;
-  const uint32_t b0 = A.bstart[k], b1 = A.bstart[k + 1];
-  const uint32_t r0 = A.binoff[b0];
-  const uint32_t r1 = b1 < A.nbins ? A.binoff[b1] : A.pairs;
-  const uint32_t n = r1 - r0;
-  const KT* __restrict__ rkey = reinterpret_cast<const KT*>(A.rkey) + r0;
-  const uint64_t* __restrict__ rid = A.rid + r0;
-  if (n > (uint32_t)kBucketCap) {  // one large fine bin: dense mode over its key window
-    bucket_dense<KT, NL, CK>(A, S, k, rkey, rid, n);
-    return;
-  }
-  const KT kEmpty = (KT)~(KT)0;
-  // 1. records (coalesced) while the table is cleared
-  KT key[IPT];
-  uint64_t id[IPT];
-#pragma unroll
-  for (int u = 0; u < IPT; ++u) {
-    const uint32_t q = threadIdx.x + u * kBucketThreads;
-    key[u] = q < n ? rkey[q] : kEmpty;
-    id[u] = q < n ? rid[q] : 0ull;
-  }
-#pragma unroll
-  for (int u = 0; u < TPT; ++u) {
-    const uint32_t t = threadIdx.x + u * kBucketThreads;
-    S.hkey[t] = kEmpty;
-#pragma unroll
-    for (int w = 0; w < 2 * NL; ++w) S.acc[t][w] = 0;
-  }
-  __syncthreads();
-  // 2. slot per key (equal keys share a slot); the product goes straight into it
-#pragma unroll
-  for (int u = 0; u < IPT; ++u) {
-    if (key[u] == kEmpty) continue;
-    uint32_t h = bucket_hash((uint64_t)key[u]);
-    for (;;) {
-      const KT prev = cas_key(&S.hkey[h], kEmpty, key[u]);
-      if (prev == kEmpty || prev == key[u]) break;
-      h = (h + 1) & (kBucketTable - 1);
-    }
-    add_product<NL, CK>(A, S.acc[h], id[u]);
-  }
-  __syncthreads();
-  // 3. occupied slots, compacted in slot order
-  {
-    const uint32_t t0 = threadIdx.x * TPT;
-#pragma unroll
-    for (int u = 0; u < TPT; ++u) S.scan[t0 + u] = S.hkey[t0 + u] != kEmpty ? 1u : 0u;
-  }
-  const uint32_t nd = chunk_scan<TPT>(S.scan, kBucketTable, S.sh);
-  {
-    const uint32_t t0 = threadIdx.x * TPT;
-#pragma unroll
-    for (int u = 0; u < TPT; ++u) {
-      const uint32_t t = t0 + u;
-      const KT kk = S.hkey[t];
-      if (kk != kEmpty) S.sortv[S.scan[t]] = ((uint64_t)kk << 12) | t;
-    }
-  }
-  __syncthreads();
-  // 4. distinct keys in key order
-  if (nd <= kBucketThreads) {
-    // few distinct keys (the common case): rank = number of smaller keys
-    uint64_t mine = 0;
-    uint32_t rank = 0;
-    if (threadIdx.x < nd) {
-      mine = S.sortv[threadIdx.x];
-      for (uint32_t x = 0; x < nd; ++x) rank += S.sortv[x] < mine ? 1u : 0u;
-    }
-    __syncthreads();
-    if (threadIdx.x < nd) S.sortv[rank] = mine;
-    __syncthreads();
-  } else {
-    uint32_t p2 = 1;
-    while (p2 < nd) p2 <<= 1;
-    for (uint32_t t = nd + threadIdx.x; t < p2; t += blockDim.x) S.sortv[t] = ~0ull;
-    __syncthreads();
-    for (uint32_t size = 2; size <= p2; size <<= 1) {
-      for (uint32_t stride = size >> 1; stride > 0; stride >>= 1) {
-        for (uint32_t t = threadIdx.x; t < p2 / 2; t += blockDim.x) {
-          const uint32_t lo = 2 * t - (t & (stride - 1));
-          const uint32_t hi = lo + stride;
-          const bool up = (lo & size) == 0;
-          const uint64_t x = S.sortv[lo], y = S.sortv[hi];
-          if ((x > y) == up) {
-            S.sortv[lo] = y;
-            S.sortv[hi] = x;
-          }
-        }
-        __syncthreads();
+  for (int e = 0; e < E; ++e) {
+    if ((e & S) == 0) {
+      const bool up = ((t * E + e) & k) == 0;
+      const uint64_t a = v[e], b = v[e + S];
+      if ((a > b) == up) {
+        v[e] = b;
+        v[e + S] = a;
       }
     }
   }
-  // 5. nonzero sums (merge.py:63) in key order -> staging
-  for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x)
-    S.scan[r] = acc_nonzero<NL, CK>(S.acc[S.sortv[r] & 0xfff]) ? 1u : 0u;
+}
+
+// strides below E inside a thread, below 32E across lanes (shuffles), larger
+// ones through `xch` (>= 256*E words of shared memory)
+template <int E>
+__device__ void block_bitonic(uint64_t (&v)[E], uint64_t* xch) {
+  constexpr uint32_t N = kBucketThreads * E;
+  const uint32_t t = threadIdx.x;
+#pragma unroll 1
+  for (uint32_t k = 2; k <= N; k <<= 1) {
+#pragma unroll 1
+    for (uint32_t s = k >> 1; s > 0; s >>= 1) {
+      if (s >= 32u * E) {
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) xch[t * E + e] = v[e];
+        __syncthreads();
+#pragma unroll
+        for (int e = 0; e < E; ++e) bitonic_keep(v[e], xch[(t * E + e) ^ s], t * E + e, s, k);
+      } else if (s >= (uint32_t)E) {
+        const int ld = (int)(s / E);
+#pragma unroll
+        for (int e = 0; e < E; ++e)
+          bitonic_keep(v[e], __shfl_xor_sync(0xffffffffu, v[e], ld), t * E + e, s, k);
+      } else {
+        if constexpr (E >= 8) {
+          if (s == 4) bitonic_reg<E, 4>(v, t, k);
+        }
+        if constexpr (E >= 4) {
+          if (s == 2) bitonic_reg<E, 2>(v, t, k);
+        }
+        if constexpr (E >= 2) {
+          if (s == 1) bitonic_reg<E, 1>(v, t, k);
+        }
+      }
+    }
+  }
   __syncthreads();
-  const uint32_t nnz = chunk_scan<IPT>(S.scan, nd, S.sh);
-  const unsigned long long base = bucket_alloc(A, k, nnz, &S.base);
-  if (base == ~0ull) return;
-  for (uint32_t r = threadIdx.x; r < nd; r += blockDim.x) {
-    const uint32_t nxt = r + 1 < nd ? S.scan[r + 1] : nnz;
-    if (nxt != S.scan[r]) write_term<NL>(A, base + S.scan[r], S.sortv[r] >> 12, S.acc[S.sortv[r] & 0xfff]);
+}
+
+// key rank of every occupied slot: rank[slot] and keyr[rank]
+template <typename KT, int NL, bool ROWS, int E>
+__device__ __forceinline__ void rank_sorted(BucketSmem<KT, NL, ROWS>& S, uint32_t nd) {
+  uint64_t v[E];
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t x = threadIdx.x * E + e;
+    v[e] = x < nd ? S.sortv[x] : ~0ull;
+  }
+  block_bitonic<E>(v, S.sortv);
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const uint32_t x = threadIdx.x * E + e;
+    if (x < nd) {
+      S.rank[v[e] & ((1u << kBkSlotBits) - 1)] = (uint16_t)x;
+      S.keyr[x] = (KT)(v[e] >> kBkSlotBits);
+    }
   }
 }
 
-// ---- B5: bucket runs -> final order -------------------------------------------
-// One warp per bucket (runs average tens of terms; a CTA per bucket left most
-// of its threads idle).
-__global__ void __launch_bounds__(256)
-k_bucket_gather(const uint64_t* __restrict__ bbase, const uint32_t* __restrict__ bnnz,
-                const uint64_t* __restrict__ boff, const uint64_t* __restrict__ sexp,
-                const uint64_t* __restrict__ scoef, int nl, uint32_t nbuckets, uint64_t* __restrict__ oexp,
-                uint64_t* __restrict__ ocoef) {
-  const uint32_t k = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const int lane = threadIdx.x & 31;
-  if (k >= nbuckets) return;
-  const uint32_t n = bnnz[k];
-  const uint64_t src = bbase[k], dst = boff[k];
-  for (uint32_t t = lane; t < n; t += 32) oexp[dst + t] = sexp[src + t];
-  for (uint32_t t = lane; t < n * (uint32_t)nl; t += 32) ocoef[dst * nl + t] = scoef[src * nl + t];
+// counting rank (threads 32.., C keys each): the number of smaller distinct keys
+template <typename KT, int NL, bool ROWS, int C>
+__device__ __forceinline__ void rank_counting(BucketSmem<KT, NL, ROWS>& S, uint32_t nd) {
+  const uint32_t t = threadIdx.x - 32;
+  KT mine[C];
+  uint32_t rk[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const uint32_t x = t + c * kBkRankThreads;
+    mine[c] = x < nd ? (KT)(S.sortv[x] >> kBkSlotBits) : (KT)~(KT)0;
+    rk[c] = 0;
+  }
+  // the keys, narrowed to KT, were stored in keyr[] in slot order by the caller
+  if constexpr (sizeof(KT) == 4) {
+    // o < mine <=> o - mine borrows: two instructions per comparison
+    uint32_t neg[C];
+#pragma unroll
+    for (int c = 0; c < C; ++c) neg[c] = 0;
+#pragma unroll 4
+    for (uint32_t y = 0; y < nd; ++y) {
+      const uint32_t o = (uint32_t)S.keyr[y];
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        uint32_t tmp;
+        asm("sub.cc.u32 %0, %2, %3;\n\tsubc.u32 %1, %1, 0;" : "=r"(tmp), "+r"(neg[c]) : "r"(o), "r"((uint32_t)mine[c]));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < C; ++c) rk[c] = 0u - neg[c];
+  } else {
+    for (uint32_t y = 0; y < nd; ++y) {
+      const KT o = S.keyr[y];
+#pragma unroll
+      for (int c = 0; c < C; ++c) rk[c] += o < mine[c] ? 1u : 0u;
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const uint32_t x = t + c * kBkRankThreads;
+    if (x < nd) S.rank[S.sortv[x] & ((1u << kBkSlotBits) - 1)] = (uint16_t)rk[c];
+  }
 }
+
+// decoupled look-back (warp 0): publish this bucket's distinct-key count,
+// return the exclusive prefix of the counts of the buckets before it.  The
+// warp reads 32 predecessors per round trip: it consumes the aggregates up to
+// the nearest inclusive prefix, or up to the first predecessor not yet
+// published (re-polled from there).
+__device__ __forceinline__ unsigned long long bucket_lookback(unsigned long long* status, uint32_t k,
+                                                              uint32_t agg) {
+  const int lane = threadIdx.x & 31;
+  volatile unsigned long long* st = status + k;
+  if (k == 0) {
+    if (lane == 0) *st = kBkPre | agg;
+    return 0;
+  }
+  if (lane == 0) *st = kBkAgg | agg;
+  unsigned long long excl = 0;
+  int64_t q = (int64_t)k - 1;  // nearest predecessor not yet consumed
+  for (;;) {
+    const int64_t idx = q - lane;
+    const unsigned long long v =
+        idx >= 0 ? *(volatile unsigned long long*)(status + idx) : (unsigned long long)kBkPre;
+    const unsigned long long flag = v & ~kBkVal;
+    const unsigned pre = __ballot_sync(0xffffffffu, flag == kBkPre);
+    const unsigned notready = __ballot_sync(0xffffffffu, flag == 0);
+    const int first_pre = pre ? __ffs(pre) - 1 : 32;
+    const unsigned upto = first_pre == 32 ? 0xffffffffu : ((2u << first_pre) - 1u);
+    const unsigned wait = notready & upto;
+    // lanes [0, take) are consumed: published aggregates, plus the prefix if no gap
+    const int take = wait ? __ffs(wait) - 1 : (first_pre == 32 ? 32 : first_pre + 1);
+    unsigned long long part = lane < take ? (v & kBkVal) : 0ull;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+    excl += part;
+    q -= take;
+    if (!wait && first_pre < 32) break;
+  }
+  if (lane == 0) *st = kBkPre | (excl + agg);
+  return excl;
+}
+
+// CK: 0 f64, 1 int64, 2 int128 operands; NL result limbs
+#ifndef PGPU_BUCKET_MINB
+#define PGPU_BUCKET_MINB (768 / PGPU_BUCKET_THREADS)
+#endif
+template <typename KT, int NL, int CK>
+__global__ void __launch_bounds__(kBucketThreads, NL <= 2 ? PGPU_BUCKET_MINB : (PGPU_BUCKET_MINB * 2 + 2) / 3)
+k_bucket_reduce(BucketArgs A) {
+  constexpr bool ROWS = CK == 0;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  BucketSmem<KT, NL, ROWS>& S = *reinterpret_cast<BucketSmem<KT, NL, ROWS>*>(smem_raw);
+  const KT kEmpty = (KT)~(KT)0;
+  for (;;) {
+    __syncthreads();  // the previous bucket's readers are done with the shared state
+    if (threadIdx.x == 0) S.bucket = atomicAdd(A.ticket, 1u);
+#pragma unroll
+    for (int u = 0; u < kBkTable / kBucketThreads; ++u) S.hkey[threadIdx.x + u * kBucketThreads] = kEmpty;
+    for (uint32_t x = threadIdx.x; x <= (uint32_t)kBucketCap; x += kBucketThreads) S.start[x] = 0;
+    __syncthreads();
+    const uint32_t k = S.bucket;
+    if (k >= A.nbuckets) return;
+    const uint32_t b0 = A.bstart[k], b1 = A.bstart[k + 1];
+    const uint32_t r0 = A.binoff[b0];
+    const uint32_t r1 = b1 < A.nbins ? A.binoff[b1] : A.pairs;
+    const uint32_t n = r1 - r0;
+    if (n > (uint32_t)kBucketCap) {  // one fine bin above the bucket bound
+      if (threadIdx.x == 0) {
+        *A.overflow = 1u;
+        volatile unsigned long long* st = A.status + k;
+        *st = (k == 0 ? kBkPre : kBkAgg) | 0ull;
+      }
+      continue;
+    }
+    // records (coalesced), 1. slot per distinct key
+    uint64_t id[kBkIpt];
+    uint32_t slot[kBkIpt];
+    uint32_t valid = 0;
+    {
+      const KT* __restrict__ rkey = reinterpret_cast<const KT*>(A.rkey) + r0;
+      const uint64_t* __restrict__ rid = A.rid + r0;
+      KT key[kBkIpt];
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u) {
+        const uint32_t q = threadIdx.x + u * kBucketThreads;
+        key[u] = q < n ? rkey[q] : kEmpty;
+        id[u] = q < n ? rid[q] : 0ull;
+        valid |= (q < n ? 1u : 0u) << u;
+      }
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u) {
+        uint32_t h = 0;
+        if ((valid >> u) & 1u) {
+          h = bucket_hash((uint64_t)key[u]);
+          for (;;) {
+            const KT prev = cas_key(&S.hkey[h], kEmpty, key[u]);
+            if (prev == kEmpty || prev == key[u]) break;
+            h = (h + 1) & (kBkTable - 1);
+          }
+        }
+        slot[u] = h;
+      }
+    }
+    __syncthreads();
+    // 2. distinct keys compacted in slot order (thread t scans slots [16t, 16t+16))
+    constexpr int TPT = kBkTable / kBucketThreads;
+    uint32_t nd;
+    {
+      const uint32_t t0 = threadIdx.x * TPT;
+      uint32_t occ = 0, cnt = 0;
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        const bool o = S.hkey[t0 + u] != kEmpty;
+        occ |= (o ? 1u : 0u) << u;
+        cnt += o ? 1u : 0u;
+      }
+      uint32_t at = block_excl_scan(cnt, S.sh, &nd);
+#pragma unroll
+      for (int u = 0; u < TPT; ++u) {
+        if ((occ >> u) & 1u) {
+          const KT kk = S.hkey[t0 + u];
+          S.sortv[at] = ((uint64_t)kk << kBkSlotBits) | (t0 + u);
+          S.keyr[at] = kk;  // slot order (counting rank input); rank order after step 3
+          ++at;
+        }
+      }
+    }
+    __syncthreads();
+    // 3. output base (warp 0, look-back) while the other warps rank the keys
+    if (nd <= 2u * kBkRankThreads) {
+      if (threadIdx.x < 32) {
+        const unsigned long long b = bucket_lookback(A.status, k, nd);
+        if (threadIdx.x == 0) S.base = b;
+      } else if (nd <= kBkRankThreads) {
+        rank_counting<KT, NL, ROWS, 1>(S, nd);
+      } else {
+        rank_counting<KT, NL, ROWS, 2>(S, nd);
+      }
+      __syncthreads();
+      // keys in rank order (keyr held them in slot order for the counting rank)
+      constexpr int RC = (2 * kBkRankThreads + kBucketThreads - 1) / kBucketThreads;
+      KT kk[RC];
+      uint32_t rk[RC];
+#pragma unroll
+      for (int c = 0; c < RC; ++c) {
+        const uint32_t x = threadIdx.x + c * kBucketThreads;
+        if (x < nd) {
+          kk[c] = S.keyr[x];
+          rk[c] = S.rank[S.sortv[x] & ((1u << kBkSlotBits) - 1)];
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int c = 0; c < RC; ++c)
+        if (threadIdx.x + c * kBucketThreads < nd) S.keyr[rk[c]] = kk[c];
+    } else {
+      if (threadIdx.x < 32) {
+        const unsigned long long b = bucket_lookback(A.status, k, nd);
+        if (threadIdx.x == 0) S.base = b;
+      }
+      if (nd <= 4u * kBucketThreads) rank_sorted<KT, NL, ROWS, 4>(S, nd);
+      else rank_sorted<KT, NL, ROWS, 8>(S, nd);
+    }
+    __syncthreads();
+    // 4. runs: count per key rank (the index is an arbitrary position in the run)
+    uint32_t pos[kBkIpt];
+#pragma unroll
+    for (int u = 0; u < kBkIpt; ++u) {
+      if ((valid >> u) & 1u) {
+        slot[u] = S.rank[slot[u]];  // slot -> key rank
+        pos[u] = atomicAdd(&S.start[slot[u]], 1u);
+      }
+    }
+    if (threadIdx.x == 0) S.start[nd] = n;
+    __syncthreads();
+    chunk_scan<kBkIpt>(S.start, nd, S.sh);
+    // position in (key, row) order
+    if constexpr (ROWS) {
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u)
+        if ((valid >> u) & 1u) S.rows[S.start[slot[u]] + pos[u]] = (uint32_t)(id[u] >> 32);
+      __syncthreads();
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u) {
+        if ((valid >> u) & 1u) {
+          const uint32_t s0 = S.start[slot[u]], len = S.start[slot[u] + 1] - s0;
+          const uint32_t i = (uint32_t)(id[u] >> 32);
+          uint32_t below = 0;
+          for (uint32_t x = 0; x < len; ++x) below += S.rows[s0 + x] < i ? 1u : 0u;
+          pos[u] = s0 + below;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u)
+        if ((valid >> u) & 1u) pos[u] += S.start[slot[u]];
+    }
+    // 5. products at their positions (sortv is dead: the ranks are in rank[]/keyr[])
+#pragma unroll
+    for (int u = 0; u < kBkIpt; ++u) {
+      if (!((valid >> u) & 1u)) continue;
+      const uint64_t i = id[u] >> 32, j = id[u] & 0xffffffffu;
+      if constexpr (CK == 0) {
+        const double pr = __dmul_rn(__ldg(reinterpret_cast<const double*>(A.ac) + i),
+                                    __ldg(reinterpret_cast<const double*>(A.bc) + j));
+        S.prod[pos[u]] = (uint64_t)__double_as_longlong(pr);
+      } else {
+        const Limbs<NL> pr = imul<NL, CK>(load_icoef<CK>(A.ac, (int64_t)i), load_icoef<CK>(A.bc, (int64_t)j));
+#pragma unroll
+        for (int w = 0; w < NL; ++w) S.prod[(size_t)pos[u] * NL + w] = pr.w[w];
+      }
+    }
+    __syncthreads();
+    // 6. one owner per key folds its run in order and writes term base + rank
+    const unsigned long long base = S.base;
+    uint32_t nzero = 0;
+    for (uint32_t r = threadIdx.x; r < nd; r += kBucketThreads) {
+      const uint32_t s0 = S.start[r], s1 = S.start[r + 1];
+      bool nz;
+      uint64_t out[NL];
+      if constexpr (CK == 0) {
+        double acc = __longlong_as_double((long long)S.prod[s0]);
+        for (uint32_t x = s0 + 1; x < s1; ++x) acc = __dadd_rn(acc, __longlong_as_double((long long)S.prod[x]));
+        out[0] = (uint64_t)__double_as_longlong(acc);
+        nz = acc != 0.0;  // NaN kept, +-0 dropped (merge.py:63)
+      } else {
+        Limbs<NL> acc;
+#pragma unroll
+        for (int w = 0; w < NL; ++w) acc.w[w] = S.prod[(size_t)s0 * NL + w];
+        for (uint32_t x = s0 + 1; x < s1; ++x) {
+          Limbs<NL> p;
+#pragma unroll
+          for (int w = 0; w < NL; ++w) p.w[w] = S.prod[(size_t)x * NL + w];
+          limbs_add(acc, p);
+        }
+#pragma unroll
+        for (int w = 0; w < NL; ++w) out[w] = acc.w[w];
+        nz = limbs_nonzero(acc);
+      }
+      const uint64_t o = base + r;
+      A.oexp[o] = nz ? expand_key(A.KL + (uint64_t)S.keyr[r], A.P) : ~0ull;
+#pragma unroll
+      for (int w = 0; w < NL; ++w) A.ocoef[o * NL + w] = out[w];
+      nzero += nz ? 0u : 1u;
+    }
+    if (nzero) atomicAdd(A.zeros, (unsigned long long)nzero);
+  }
+}
+
+// terms present (not a zero-sum hole marked by the all-ones exponent)
+struct HoleGen {
+  const uint64_t* exps;
+  __device__ uint32_t operator()(uint64_t i) const { return exps[i] != ~0ull ? 1u : 0u; }
+};
 
 // bin offsets (exclusive scan of the fine-bin histogram)
 struct BinOffOut {
@@ -490,15 +655,6 @@ struct BinOffOut {
 struct HistGen {
   const uint32_t* hist;
   __device__ uint32_t operator()(uint64_t b) const { return hist[b]; }
-};
-
-struct BnnzGen {
-  const uint32_t* bnnz;
-  __device__ uint64_t operator()(uint64_t k) const { return bnnz[k]; }
-};
-struct BoffOut {
-  uint64_t* boff;
-  __device__ void operator()(uint64_t k, uint64_t ex, uint64_t) const { boff[k] = ex; }
 };
 
 }  // namespace pgpu

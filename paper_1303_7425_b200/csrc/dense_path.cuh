@@ -551,11 +551,19 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
       return nv;
     };
     auto rows = [&](auto tbl_mode) {
-      // warps claim 32-row groups dynamically (one shared counter per interval)
-      for (;;) {
-        uint32_t g = 0;
-        if (lane == 0) g = atomicAdd(&row_ctr, (uint32_t)kRowClaim);
-        g = rb0 + __shfl_sync(0xffffffffu, g, 0);
+      // integers: warps claim 32-row groups dynamically (one shared counter per
+      // interval; exact sums do not depend on which copy a row lands in).
+      // f64: static groups w, w + W, w + 2W, ... so every run folds the same
+      // rows into the same warp copy and the sums are bit-identical run to run
+      for (uint32_t it = 0;; ++it) {
+        uint32_t g;
+        if constexpr (MODE == 0) {
+          g = rb0 + (w + it * kNumWarps) * kRowClaim;
+        } else {
+          g = 0;
+          if (lane == 0) g = atomicAdd(&row_ctr, (uint32_t)kRowClaim);
+          g = rb0 + __shfl_sync(0xffffffffu, g, 0);
+        }
         if (g >= rb1) break;
         const uint32_t i = g + lane;
         const bool rowok = lane < kRowClaim && i < rb1;

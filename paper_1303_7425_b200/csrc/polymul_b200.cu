@@ -22,6 +22,7 @@
 #include <cstring>
 #include <map>
 #include <mutex>
+#include <set>
 #include <string>
 #include <vector>
 
@@ -103,6 +104,52 @@ int device_setup(int dev, cudaStream_t* st) {
   *st = d.stream;
   return PGPU_OK;
 }
+
+// Kernel attributes are per device context: the opt-in shared-memory size is
+// set once per (kernel, device), and occupancy queries are cached per kernel.
+std::mutex g_attr_mu;
+std::set<std::pair<const void*, int>> g_attr_done;
+std::map<std::pair<const void*, size_t>, int> g_occ;
+
+template <typename K>
+void smem_attr(K kern, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  if (g_attr_done.insert({(const void*)kern, dev}).second)
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+}
+
+// resident CTAs per SM (>= 1)
+template <typename K>
+int occupancy(K kern, int threads, size_t smem) {
+  std::lock_guard<std::mutex> lk(g_attr_mu);
+  auto it = g_occ.find({(const void*)kern, smem});
+  if (it != g_occ.end()) return it->second;
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, threads, smem) != cudaSuccess) {
+    cudaGetLastError();
+    per_sm = 1;
+  }
+  per_sm = std::max(per_sm, 1);
+  g_occ[{(const void*)kern, smem}] = per_sm;
+  return per_sm;
+}
+
+// The ABI never leaves the caller's thread on another device (torch keeps its
+// own notion of the current device).
+struct DeviceRestore {
+  int prev = -1;
+  DeviceRestore() {
+    if (cudaGetDevice(&prev) != cudaSuccess) {
+      cudaGetLastError();
+      prev = -1;
+    }
+  }
+  ~DeviceRestore() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 constexpr size_t kWorkspaceMaxItem = 1ull << 30;  // larger buffers bypass the workspace
 constexpr size_t kWorkspaceMax = 16ull << 30;     // workspace never grows beyond this
@@ -220,6 +267,7 @@ struct PinnedPool {
       cudaGetLastError();
       return nullptr;
     }
+    std::lock_guard<std::mutex> lk(mu);  // put() may run concurrently (no device lock there)
     sizes_[p] = bytes;
     return p;
   }
@@ -236,6 +284,23 @@ struct PinnedPool {
 };
 PinnedPool g_pinned;
 constexpr uintptr_t kPinnedTag = 0x50494e4e;  // result buffers come from g_pinned
+constexpr uintptr_t kDevTag = 0x44455600;     // device result: kDevTag | device ordinal
+
+// stream-ordered free of a device result on its own device's library stream
+void free_device_ptr(void* p, void* owner) {
+  if (!p) return;
+  const uintptr_t tag = (uintptr_t)owner;
+  if ((tag & ~uintptr_t(0xff)) == kDevTag) {
+    const int dev = (int)(tag & 0xff);
+    DeviceRestore dr;
+    if (cudaSetDevice(dev) == cudaSuccess && g_dev[dev & 63].init) {
+      cudaFreeAsync(p, g_dev[dev & 63].stream);
+      return;
+    }
+    cudaGetLastError();
+  }
+  cudaFreeAsync(p, 0);
+}
 
 struct Timer {
   bool on = false;
@@ -285,6 +350,7 @@ struct Ctx {
   Timer tm;
   int64_t launches = 0;
   int sms = 148;
+  int device = 0;
 };
 
 inline int grid_for(int64_t n, int threads, int cap) {
@@ -374,14 +440,38 @@ int count_at(Ctx& ctx, const Problem& pb, const std::vector<uint64_t>& bounds,
 // Bucket path driver (kernels in bucket_path.cuh)
 #include "bucket_driver.inc"
 
+// Memory this process can still use on device `dev`: free device memory plus
+// what the stream-ordered pool holds reserved but unused (it retains freed
+// blocks).  Queried only for large products: cudaMemGetInfo can stall.
+size_t fresh_budget(int dev) {
+  size_t f = 0, t = 0;
+  if (cudaMemGetInfo(&f, &t) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaMemPool_t pool;
+  uint64_t res = 0, used = 0;
+  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReservedMemCurrent, &res);
+    cudaMemPoolGetAttribute(pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  } else {
+    cudaGetLastError();
+  }
+  return f + (res > used ? (size_t)(res - used) : 0);
+}
+
 template <typename KT>
 int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice>& slices,
-                  bool try_bucket, int* nbucket) {
-  const size_t freeb = ctx.mem_budget;
+                  bool try_bucket, int* nbucket, double cap_scale = 1.0) {
   // per pair: records x2 (key + i<<32|j), segment starts; the segment outputs
   // (<= pairs, usually far fewer) and scan scratch fit in the remaining slack
   uint64_t bpp = 2 * (sizeof(KT) + 8) + 4 + 8;
-  uint64_t cap = (uint64_t)(freeb * 0.55) / bpp;
+  size_t freeb = ctx.mem_budget;
+  if (total * bpp > freeb / 8) {  // large product: the budget cached at first use may be stale
+    const size_t now = fresh_budget(ctx.device);
+    if (now) freeb = now;
+  }
+  uint64_t cap = (uint64_t)(freeb * 0.55 * cap_scale) / bpp;
   if (cap > (1ull << 31)) cap = 1ull << 31;  // 32-bit positions inside a batch
   const char* env = getenv("PGPU_BATCH_CAP");
   if (env) cap = std::min<uint64_t>(cap, strtoull(env, nullptr, 10));
@@ -681,6 +771,7 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   TRY(device_setup(o.device, &lib_st));
   Ctx ctx;
   ctx.st = o.stream ? (cudaStream_t)o.stream : lib_st;
+  ctx.device = o.device;
   CUDA_TRY(cudaDeviceGetAttribute(&ctx.sms, cudaDevAttrMultiProcessorCount, o.device));
   DeviceState& dstate = g_dev[o.device & 63];
   std::lock_guard<std::mutex> ws_lock(dstate.mu);
@@ -725,17 +816,15 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   if (pb.KL < pb.KH) {
     // total pairs in range
     uint64_t total = (uint64_t)pb.na * pb.nb;
-    if (pb.KL > pb.kmin || pb.KH <= pb.kmax) {
+    if (o.range_pairs > 0) {
+      total = (uint64_t)o.range_pairs;  // the caller's plan (a previous result's pair count)
+    } else if (pb.KL > pb.kmin || pb.KH <= pb.kmax) {
+      // pairs below both ends of the range in one count (one round trip)
       std::vector<uint64_t> bb{pb.KL}, cb;
+      if (pb.KH != ~0ull) bb.push_back(pb.KH);
       if (pb.k32) TRY(count_at<uint32_t>(ctx, pb, bb, cb)); else TRY(count_at<uint64_t>(ctx, pb, bb, cb));
-      uint64_t below_lo = cb[0];
-      uint64_t below_hi = (uint64_t)pb.na * pb.nb;
-      if (pb.KH != ~0ull) {
-        std::vector<uint64_t> bh{pb.KH}, ch;
-        if (pb.k32) TRY(count_at<uint32_t>(ctx, pb, bh, ch)); else TRY(count_at<uint64_t>(ctx, pb, bh, ch));
-        below_hi = ch[0];
-      }
-      total = below_hi - below_lo;
+      const uint64_t below_hi = pb.KH != ~0ull ? cb[1] : (uint64_t)pb.na * pb.nb;
+      total = below_hi - cb[0];
     }
     out->pairs = (int64_t)total;
     ctx.tm.mark(0, "prep");
@@ -753,8 +842,24 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
       const bool bucket = !(o.float_ordered && o.coef_kind == PGPU_F64) && o.path != PGPU_PATH_SORT &&
                           !getenv("PGPU_NO_BUCKET");
       int nbucket = 0;
-      if (pb.k32) TRY(run_sort_path<uint32_t>(ctx, pb, total, slices, bucket, &nbucket));
-      else TRY(run_sort_path<uint64_t>(ctx, pb, total, slices, bucket, &nbucket));
+      int r = PGPU_OK;
+      for (double scale = 1.0; scale >= 0.25; scale *= 0.5) {
+        // out of memory (other users of the device): retry with smaller batches
+        for (auto& sl : slices)
+          for (void* q : {(void*)sl.exps, (void*)sl.coef})
+            if (ar.owns(q)) {
+              ar.release(q);
+              cudaFreeAsync(q, ctx.st);
+            }
+        slices.clear();
+        nbucket = 0;
+        if (pb.k32) r = run_sort_path<uint32_t>(ctx, pb, total, slices, bucket, &nbucket, scale);
+        else r = run_sort_path<uint64_t>(ctx, pb, total, slices, bucket, &nbucket, scale);
+        if (r != PGPU_ENOMEM) break;
+        cudaGetLastError();
+        cudaStreamSynchronize(ctx.st);
+      }
+      TRY(r);
       if (nbucket > 0) used = PGPU_PATH_BUCKET;
     }
     out->path_used = used;
@@ -785,6 +890,7 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
     ar.release(c);
     out->exps = e;
     out->coeffs = c;
+    out->_owner = (void*)(kDevTag | (uintptr_t)(o.device & 0xff));
   } else {
     out->exps = (uint64_t*)g_pinned.get(std::max<uint64_t>(n, 1) * 8);
     out->coeffs = g_pinned.get(std::max<uint64_t>(n, 1) * 8 * nl);
@@ -821,6 +927,7 @@ void pgpu_default_options(pgpu_options* o) {
 
 int pgpu_mul(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
              const pgpu_options* opt, pgpu_result* out) {
+  DeviceRestore dr;
   int r = mul_impl(a, b, lay, opt, out);
   if (r != PGPU_OK && out) {
     // release anything already handed to the result
@@ -840,6 +947,7 @@ int pgpu_count_below(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* 
     for (int64_t k = 0; k < nbounds; ++k) cum[k] = 0;
     return PGPU_OK;
   }
+  DeviceRestore dr;
   cudaStream_t lib_st;
   TRY(device_setup(o.device, &lib_st));
   Ctx ctx;
@@ -866,10 +974,10 @@ int pgpu_count_below(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* 
 void pgpu_free_result(pgpu_result* r) {
   if (!r) return;
   if (r->on_device) {
-    // stream-ordered free on the legacy default stream: the memory goes back to
-    // the (retained) pool for the next product instead of to the driver
-    if (r->exps) cudaFreeAsync(r->exps, 0);
-    if (r->coeffs) cudaFreeAsync(r->coeffs, 0);
+    // stream-ordered free on the owning device's stream: the memory goes back
+    // to the (retained) pool for the next product instead of to the driver
+    free_device_ptr(r->exps, r->_owner);
+    free_device_ptr(r->coeffs, r->_owner);
   } else if (r->_owner == (void*)kPinnedTag) {
     if (r->exps) g_pinned.put(r->exps);
     if (r->coeffs) g_pinned.put(r->coeffs);
@@ -884,6 +992,7 @@ void pgpu_free_result(pgpu_result* r) {
 
 int pgpu_format(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64_t end,
                 const pgpu_options* opt, pgpu_text* out) {
+  DeviceRestore dr;
   int r = format_impl(p, lay, begin, end, opt, out);
   if (r != PGPU_OK && out) pgpu_free_text(out);
   return r;
@@ -891,7 +1000,7 @@ int pgpu_format(const pgpu_poly* p, const pgpu_layout* lay, int64_t begin, int64
 
 void pgpu_free_text(pgpu_text* t) {
   if (!t || !t->text) return;
-  if (t->on_device) cudaFreeAsync(t->text, 0);
+  if (t->on_device) free_device_ptr(t->text, t->_owner);
   else if (t->_owner == (void*)kPinnedTag) g_pinned.put(t->text);
   else free(t->text);
   t->text = nullptr;
@@ -900,6 +1009,7 @@ void pgpu_free_text(pgpu_text* t) {
 
 int pgpu_ipc_alloc(int64_t bytes, int32_t device, void** dptr, void* handle) {
   if (!dptr || !handle || bytes < 0) return fail(PGPU_EINVAL, "null argument");
+  DeviceRestore dr;
   CUDA_TRY(cudaSetDevice(device));
   *dptr = nullptr;
   // plain cudaMalloc: stream-ordered pool memory is not IPC-shareable by default
@@ -919,6 +1029,7 @@ int pgpu_ipc_alloc(int64_t bytes, int32_t device, void** dptr, void* handle) {
 
 int pgpu_ipc_open(const void* handle, int32_t device, void** dptr) {
   if (!dptr || !handle) return fail(PGPU_EINVAL, "null argument");
+  DeviceRestore dr;
   CUDA_TRY(cudaSetDevice(device));
   cudaIpcMemHandle_t h;
   memcpy(&h, handle, sizeof h);
@@ -939,6 +1050,7 @@ int pgpu_ipc_free(void* dptr) {
 int pgpu_copy(void* dst, const void* src, int64_t bytes, int32_t device, void* stream) {
   if (bytes <= 0) return PGPU_OK;
   if (!dst || !src) return fail(PGPU_EINVAL, "null argument");
+  DeviceRestore dr;
   cudaStream_t lib_st;
   TRY(device_setup(device, &lib_st));
   CUDA_TRY(cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDeviceToDevice,
@@ -947,6 +1059,7 @@ int pgpu_copy(void* dst, const void* src, int64_t bytes, int32_t device, void* s
 }
 
 int pgpu_stream_sync(int32_t device, void* stream) {
+  DeviceRestore dr;
   cudaStream_t lib_st;
   TRY(device_setup(device, &lib_st));
   CUDA_TRY(cudaStreamSynchronize(stream ? (cudaStream_t)stream : lib_st));

@@ -128,8 +128,12 @@ def evaluate(node, layout, ctype=int, mul=None):
     mul_arrays): no Python int is built until the final result."""
     if mul is None:
         from .arrays import ArrayPolynomial
-        from .parmul import mul_arrays
-        out = _evaluate(node, layout, ctype, mul_arrays)
+        from .parmul import MulConfig, mul_arrays
+        # float operands are built in the reference's summation order (its
+        # default multiplier folds rows in increasing i), so they are the
+        # reference's operands bit for bit, not just within tolerance
+        cfg = MulConfig(float_ordered=ctype is float)
+        out = _evaluate(node, layout, ctype, lambda x, y: mul_arrays(x, y, cfg))
         return out.to_poly() if isinstance(out, ArrayPolynomial) else out
     return _evaluate(node, layout, ctype, mul)
 

@@ -53,7 +53,7 @@ def test_ctypes_struct_layouts_match_c(tmp_path):
 #include "{HEADER}"
 int main(void) {{
   printf("%zu %zu %zu %zu %zu\\n", sizeof(pgpu_layout), sizeof(pgpu_poly), sizeof(pgpu_options), sizeof(pgpu_result), sizeof(pgpu_text));
-  printf("%zu %zu %zu\\n", offsetof(pgpu_options, lo), offsetof(pgpu_options, stream), offsetof(pgpu_result, phase_ms));
+  printf("%zu %zu %zu %zu\\n", offsetof(pgpu_options, lo), offsetof(pgpu_options, stream), offsetof(pgpu_result, phase_ms), offsetof(pgpu_options, range_pairs));
   return 0;
 }}''')
     exe = tmp_path / "sz"
@@ -63,12 +63,13 @@ int main(void) {{
     assert sizes == [C.sizeof(N.Layout), C.sizeof(N.Poly), C.sizeof(N.Options), C.sizeof(N.Result),
                      C.sizeof(N.Text)]
     offs = [int(x) for x in lines[1].split()]
-    assert offs == [N.Options.lo.offset, N.Options.stream.offset, N.Result.phase_ms.offset]
+    assert offs == [N.Options.lo.offset, N.Options.stream.offset, N.Result.phase_ms.offset,
+                    N.Options.range_pairs.offset]
 
 
 def test_library_answers_without_a_gpu():
     lib = N.load()
-    assert lib.pgpu_abi_version() == 2
+    assert lib.pgpu_abi_version() == 3
     assert lib.pgpu_device_count() >= 0
     o = N.default_options()
     assert o.hi == (1 << 64) - 1 and o.lo == 0 and o.coef_kind == N.F64

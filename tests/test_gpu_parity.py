@@ -78,12 +78,60 @@ def test_float_fast_mode_within_bound(name):
     fast = mul(f, g, MulConfig(path="auto"))
     exact = mul(f, g, MulConfig(float_ordered=True))
     assert fast.exps == exact.exps
-    # all-positive operands: sum|a_i b_j| == the coefficient itself; k <= min(na, nb)
-    k = min(f.n, g.n)
+    # all-positive operands: sum|a_i b_j| == the coefficient itself.  k is the
+    # term's own product count (rtol 2k*2^-53, k <= 17,151 on F30),
+    # counted exactly on the GPU as the product of the all-ones supports
+    ones_f = Polynomial._from_sorted(f.layout, f.exps, [1] * f.n, int)
+    ones_g = Polynomial._from_sorted(g.layout, g.exps, [1] * g.n, int)
+    cnt = mul(ones_f, ones_g)
+    assert cnt.exps == exact.exps and sum(cnt.coeffs) == f.n * g.n
+    k = np.asarray(cnt.coeffs, dtype=np.float64)
     x = np.asarray(fast.coeffs)
     y = np.asarray(exact.coeffs)
     bound = 2 * k * 2.0 ** -53 * np.abs(y)
     assert np.all(np.abs(x - y) <= bound)
+    if name == "fateman30":
+        assert k.max() == 17151  # SURVEY 8(a) segment-length table
+
+
+@pytest.mark.parametrize("name,path", [("fateman20", "auto"), ("fateman30", "auto"), ("mp12", "auto"),
+                                       ("mp12", "bucket"), ("fateman20", "sort"), ("fateman10", "small")])
+def test_float_fast_mode_is_deterministic(name, path):
+    """Reference acceptance criterion 8 (test_acceptance.py:237-256):
+    repeated float products are bit-identical.  No device path may let a race
+    (row claims, atomics) decide a summation order."""
+    from paper_1303_7425_b200.parmul import mul_arrays
+    f, g = benchpolys.CONFIGS[name](float)
+    if path == "small":
+        f, g = benchpolys.fateman(2, float)
+    runs = [mul_arrays(f, g, MulConfig(path=path)) for _ in range(3)]
+    e0 = runs[0].exps_array()
+    c0 = runs[0].coef_array().view(np.uint64)
+    for r in runs[1:]:
+        assert np.array_equal(r.exps_array(), e0)
+        assert np.array_equal(r.coef_array().view(np.uint64), c0)
+
+
+def test_mp12_float_auto_equals_reference_digest():
+    """Sparse products fold each term in increasing row (the bucket path's
+    owner fold), so the default float mode is the reference's result bit for bit."""
+    f, g = benchpolys.CONFIGS["mp12"](float)
+    p = mul(f, g)
+    want = digests()["products"]["mp12/float"]
+    assert p.n == want["n"] and io.poly_digest(p) == want["sha256"]
+
+
+def test_default_float_powering_builds_reference_operands():
+    """poly_from_expr with the default (GPU) multiplier powers float operands in
+    the reference's order (its default naive_mul folds rows in increasing i)."""
+    from conftest import golden
+    from paper_1303_7425_b200.expr import poly_from_expr
+    for e in golden()["exprs"]:
+        if e["ctype"] != "float" or "^30" in e["text"]:
+            continue
+        lay = default_layout(tuple(e["vars"]))
+        p = poly_from_expr(e["text"], lay, float)
+        assert p.n == e["n"] and io.poly_digest(p) == e["sha256"], e["text"]
 
 
 def test_mp25_sampled_intervals_match_reference():
