@@ -577,7 +577,9 @@ def main():
                                            "(correctness run; times are not a scaling measurement)"
                                            if emulated else "")) if world > 1 else "1 GPU",
                           "gather": {"peer": "peer copies of disjoint slices to rank 0 (CUDA IPC, "
-                                             "NVLink); counts and completion stream-ordered over NCCL",
+                                             "NVLink); counts and completion " +
+                                             ("exchanged over gloo" if args.emulate_ranks else
+                                              "stream-ordered over NCCL"),
                                      "collective": "all-gather of disjoint slices",
                                      "none": "none (1 GPU)"}[gather_kind],
                           "l2": f"flushed ({args.flush_mib} MiB write) between timed steps",
@@ -652,6 +654,25 @@ def main():
             out["e2e"] = {"value": total_pairs / e2e_s, "unit": UNIT,
                           "h2d_bytes_per_step": h2d * world, "d2h_bytes_per_step": d2h,
                           "ms_per_step": 1e3 * e2e_s}
+        if world == 1 and out is not None:
+            # the reference-facing call: Polynomial (Python int/float lists) in,
+            # Polynomial out -- marshaling both ways inside the timed region
+            from paper_1303_7425_b200 import MulConfig, mul
+            cfg = MulConfig(path=args.path, float_ordered=False, device=local)
+            api_t = []
+            for k in range(2 + min(args.steps, 5)):
+                t1 = time.perf_counter()
+                p = mul(f, g, cfg)
+                t2 = time.perf_counter()
+                if k >= 2:
+                    api_t.append(t2 - t1)
+                del p
+            api_s = sum(api_t) / len(api_t)
+            out["e2e_api"] = {"value": total_pairs / api_s, "unit": UNIT, "ms_per_step": 1e3 * api_s,
+                              "steps": len(api_t),
+                              "call": "paper_1303_7425_b200.mul(Polynomial, Polynomial) -> Polynomial: "
+                                      "Python int lists marshaled in and out (the reference's parmul.mul "
+                                      "signature, parmul.py:91-109)"}
     if args.verify:
         out_v = verify_product(args, f, step, gathered, world, rank)
         if out is not None:

@@ -75,9 +75,10 @@ typedef enum pgpu_path {
   PGPU_PATH_AUTO = 0,
   PGPU_PATH_DENSE = 1,    /* sumset bytemap + per-interval private accumulators    */
   PGPU_PATH_SORT = 2,     /* expand / LSD radix sort / run-length reduce            */
-  PGPU_PATH_BUCKET = 3,   /* pairs written once into key-range buckets of <= 512,
-                             each grouped and reduced by one CTA in shared memory
-                             (a batch that does not suit it takes PATH_SORT)       */
+  PGPU_PATH_BUCKET = 3,   /* pairs written once into key-range buckets of <= 2048,
+                             each grouped and folded by one CTA in shared memory
+                             in (key, row) order (a batch that does not suit it
+                             takes PATH_SORT)                                      */
   PGPU_PATH_SMALL = 4     /* products of at most 16384 pairs in one CTA (sorted in
                              shared memory, folded in the reference's row order);
                              AUTO takes it for such products                        */
@@ -106,9 +107,10 @@ typedef struct pgpu_options {
   int32_t acc_limbs;                /* result int width in u64 limbs (1..3), 0 = auto */
   int32_t device;                   /* CUDA ordinal                             */
   int32_t path;                     /* pgpu_path                                */
-  int32_t float_ordered;            /* 1: fold each coefficient in the reference's
+  int32_t float_ordered;            /* 1: fold each f64 coefficient in the reference's
                                        order (increasing row i, merge.py:32-33) so
-                                       doubles are bit-identical; forces PATH_SORT */
+                                       doubles are bit-identical: small, bucket or
+                                       sort path (the dense path refuses)          */
   int32_t timing;                   /* 1: record per-phase CUDA-event times     */
   int32_t inputs_on_device;         /* 1: pgpu_poly pointers are device pointers */
   int32_t outputs_on_device;        /* 1: result stays in device memory         */

@@ -17,6 +17,9 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIBDIR = PKG / "lib"
 LIB = LIBDIR / "libpolymul_b200.so"
+# device-side bounds assertions (-DPGPU_CHECKED): the checked build the GPU
+# tests run every path through (tests/test_gpu_checked.py)
+LIB_CHECKED = LIBDIR / "libpolymul_b200_checked.so"
 ROOT = PKG.parent
 
 NVCC_FLAGS = [
@@ -40,10 +43,10 @@ def sources() -> list:
         ROOT / "include" / "polymul_b200.h"]
 
 
-def stale() -> bool:
-    if not LIB.exists():
+def stale(lib: Path = LIB) -> bool:
+    if not lib.exists():
         return True
-    t = LIB.stat().st_mtime
+    t = lib.stat().st_mtime
     return any(s.stat().st_mtime > t for s in sources())
 
 
@@ -65,6 +68,13 @@ def build(force: bool = False, verbose: bool = False, out: Path | None = None,
         print(res.stdout, res.stderr, file=sys.stderr)
     os.replace(tmp, target)
     return target
+
+
+def build_checked(force: bool = False, verbose: bool = False) -> Path:
+    """The checked library (device bounds assertions); same sources."""
+    if not force and not stale(LIB_CHECKED):
+        return LIB_CHECKED
+    return build(force=True, verbose=verbose, out=LIB_CHECKED, defines=("PGPU_CHECKED",))
 
 
 def build_pylimbs(force: bool = False) -> Path:
@@ -89,4 +99,5 @@ def build_pylimbs(force: bool = False) -> Path:
 
 if __name__ == "__main__":
     print(build(force="--force" in sys.argv, verbose=True))
+    print(build_checked(force="--force" in sys.argv))
     print(build_pylimbs(force="--force" in sys.argv))

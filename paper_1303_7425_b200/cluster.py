@@ -305,8 +305,7 @@ def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
     import torch
     import torch.distributed as dist
     from . import parmul
-    if cfg is None:
-        cfg = parmul.MulConfig()
+    cfg = parmul.MulConfig.of(cfg)
     check_compatible(a, b)
     cls = type(a)
     if a.is_zero or b.is_zero:
@@ -322,7 +321,7 @@ def gpu_mul(a, b, cfg=None, *, group=None, local_fn=None, count_fn=None):
         def local_fn(x, y, lo, hi):
             return parmul.native_mul(parmul.Operand.from_poly(x), parmul.Operand.from_poly(y),
                                      x.layout, lo=lo, hi=hi, path=cfg.path,
-                                     float_ordered=cfg.float_ordered, device=cfg.device)
+                                     float_ordered=cfg.ordered, device=cfg.device)
     bounds, plan = plan_for_ranks(a, b, cfg.l, world, rank, count_fn, group)
     lo, hi = rank_range(bounds, plan, rank)
     if device_path:
@@ -389,7 +388,7 @@ def _gpu_range_and_peer_gather(a, b, cfg, lo, hi, group):
         dA = DeviceOperand(parmul.Operand.from_poly(a), dev)
         dB = DeviceOperand(parmul.Operand.from_poly(b), dev)
         res = mul_on_device(dA, dB, a.layout, lo=lo, hi=hi, path=cfg.path,
-                            float_ordered=cfg.float_ordered, device=cfg.device)
+                            float_ordered=cfg.ordered, device=cfg.device)
     try:
         if res is not None and res.n:
             e, c = res.tensors()

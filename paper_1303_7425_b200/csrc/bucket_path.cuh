@@ -112,7 +112,8 @@ template <typename KT>
 __global__ void __launch_bounds__(256)
 k_bin_scatter(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
               const uint32_t* __restrict__ rhi, uint32_t na, uint64_t KL, BinMap map,
-              uint32_t* __restrict__ fill, KT* __restrict__ rkey, uint64_t* __restrict__ rid) {
+              uint32_t* __restrict__ fill, KT* __restrict__ rkey, uint64_t* __restrict__ rid,
+              uint64_t cap) {
   const int lane = threadIdx.x & 31;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   for (uint32_t i = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; i < na; i += nwarps) {
@@ -128,6 +129,7 @@ k_bin_scatter(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32
       uint32_t pos = 0;
       if (r.head) pos = atomicAdd(fill + bin, r.len);
       pos = __shfl_sync(0xffffffffu, pos, r.head_lane) + (uint32_t)(lane - r.head_lane);
+      PGPU_ASSERT(!valid || pos < cap);
       if (valid) {
         rkey[pos] = (KT)key;
         rid[pos] = ((uint64_t)i << 32) | j;
@@ -572,7 +574,10 @@ k_bucket_reduce(BucketArgs A) {
     if constexpr (ROWS) {
 #pragma unroll
       for (int u = 0; u < kBkIpt; ++u)
-        if ((valid >> u) & 1u) S.rows[S.start[slot[u]] + pos[u]] = (uint32_t)(id[u] >> 32);
+        if ((valid >> u) & 1u) {
+          PGPU_ASSERT(slot[u] < nd && S.start[slot[u]] + pos[u] < S.start[slot[u] + 1]);
+          S.rows[S.start[slot[u]] + pos[u]] = (uint32_t)(id[u] >> 32);
+        }
       __syncthreads();
 #pragma unroll
       for (int u = 0; u < kBkIpt; ++u) {
@@ -593,6 +598,7 @@ k_bucket_reduce(BucketArgs A) {
 #pragma unroll
     for (int u = 0; u < kBkIpt; ++u) {
       if (!((valid >> u) & 1u)) continue;
+      PGPU_ASSERT(slot[u] < nd && pos[u] >= S.start[slot[u]] && pos[u] < S.start[slot[u] + 1] && pos[u] < n);
       const uint64_t i = id[u] >> 32, j = id[u] & 0xffffffffu;
       if constexpr (CK == 0) {
         const double pr = __dmul_rn(__ldg(reinterpret_cast<const double*>(A.ac) + i),
@@ -632,6 +638,7 @@ k_bucket_reduce(BucketArgs A) {
         nz = limbs_nonzero(acc);
       }
       const uint64_t o = base + r;
+      PGPU_ASSERT(o < A.pairs && s0 < s1 && s1 <= n);
       A.oexp[o] = nz ? expand_key(A.KL + (uint64_t)S.keyr[r], A.P) : ~0ull;
 #pragma unroll
       for (int w = 0; w < NL; ++w) A.ocoef[o * NL + w] = out[w];

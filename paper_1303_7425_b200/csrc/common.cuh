@@ -13,6 +13,17 @@
 #include <cstdint>
 #include <cuda_runtime.h>
 
+// Checked build (-DPGPU_CHECKED, lib/libpolymul_b200_checked.so): device-side
+// bounds assertions on every shared-memory slot, table and output index the
+// kernels compute (a failed one traps and the call returns PGPU_ECUDA).  The
+// product build compiles them out.
+#ifdef PGPU_CHECKED
+#include <cassert>
+#define PGPU_ASSERT(c) assert(c)
+#else
+#define PGPU_ASSERT(c) ((void)0)
+#endif
+
 namespace pgpu {
 
 constexpr int kMaxFields = 15;

@@ -73,6 +73,7 @@ constexpr uint32_t kSymWin = PGPU_SYM_WIN;
 // bit 5 by bit 7 moves every other pair of blocks to the unused banks.  The map
 // is an involution inside each aligned 64-byte block.
 __device__ __forceinline__ uint32_t sym_slot(uint32_t o) {
+  PGPU_ASSERT(o < kSymWin);
   return PGPU_SYM_SWZ ? o ^ ((o >> 2) & 32u) : o;
 }
 
@@ -221,6 +222,7 @@ struct WordOut {
   uint32_t* prefix;
   OKT* okey;
   uint64_t R0;
+  uint64_t span_cap;  // key span (checked build: marks stay inside it)
   __device__ void operator()(uint64_t w, uint32_t ex, uint32_t v) const {
     uint32_t m = gen.mask(w);
     bits[w] = m;
@@ -229,6 +231,7 @@ struct WordOut {
     while (m) {
       int b = __ffs(m) - 1;
       m &= m - 1;
+      PGPU_ASSERT(R0 + w * 32 + b < R0 + span_cap);
       okey[r++] = (OKT)(R0 + w * 32 + b);
     }
   }
@@ -442,7 +445,10 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
           int b = __ffs(m) - 1;
           m &= m - 1;
           uint64_t k = A.R0 + wd * 32 + b;
-          if (k >= Klo && k < Khi) tbl[k - Klo] = (uint16_t)rk;
+          if (k >= Klo && k < Khi) {
+            PGPU_ASSERT(k - Klo < kTbl && rk < D);
+            tbl[k - Klo] = (uint16_t)rk;
+          }
           ++rk;
         }
       }
@@ -484,6 +490,7 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
           sl = ok ? rank_of<KT>((uint64_t)key - A.R0, A.bits, A.prefix) - base : 0u;
         }
         slot[u] = ok ? sl : D + lane;
+        PGPU_ASSERT(slot[u] < DP && (!ok || sl < D));
         okk[u] = ok;
       }
       if constexpr (MODE == 1 && CB) {

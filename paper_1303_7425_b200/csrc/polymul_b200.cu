@@ -467,9 +467,9 @@ int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice
   // (<= pairs, usually far fewer) and scan scratch fit in the remaining slack
   uint64_t bpp = 2 * (sizeof(KT) + 8) + 4 + 8;
   size_t freeb = ctx.mem_budget;
-  if (total * bpp > freeb / 8) {  // large product: the budget cached at first use may be stale
+  if (cap_scale < 1.0) {  // a retry after ENOMEM: the budget cached at first use was stale
     const size_t now = fresh_budget(ctx.device);
-    if (now) freeb = now;
+    if (now) freeb = std::min(freeb, now);
   }
   uint64_t cap = (uint64_t)(freeb * 0.55 * cap_scale) / bpp;
   if (cap > (1ull << 31)) cap = 1ull << 31;  // 32-bit positions inside a batch
@@ -829,18 +829,27 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
     out->pairs = (int64_t)total;
     ctx.tm.mark(0, "prep");
     int path = o.path;
-    if (o.float_ordered && o.coef_kind == PGPU_F64) path = PGPU_PATH_SORT;
+    // the reference's float order (merge.py:32-33): the bucket and sort paths
+    // fold each term in increasing row; the dense path's warp copies do not
+    const bool ordered = o.float_ordered && o.coef_kind == PGPU_F64;
+    if (ordered && path == PGPU_PATH_DENSE)
+      return fail(PGPU_EUNSUPPORTED, "float_ordered products do not take the dense path");
     int used = PGPU_PATH_SORT;
     if (path == PGPU_PATH_SMALL) path = PGPU_PATH_AUTO;  // product too large for one CTA
-    if (path != PGPU_PATH_SORT && path != PGPU_PATH_BUCKET) {
+    if (path != PGPU_PATH_SORT && path != PGPU_PATH_BUCKET && !ordered) {
       int r = dense_try(ctx, pb, total, slices, path == PGPU_PATH_DENSE, &used);
       if (r != PGPU_OK) return r;
     }
     if (used == PGPU_PATH_SORT) {
-      // sparse products: buckets per CTA; the reference-order float fold and
-      // explicit PATH_SORT keep the global radix sort
-      const bool bucket = !(o.float_ordered && o.coef_kind == PGPU_F64) && o.path != PGPU_PATH_SORT &&
-                          !getenv("PGPU_NO_BUCKET");
+      // sparse products: buckets per CTA; explicit PATH_SORT keeps the global
+      // radix sort.  Products whose keys carry thousands of pairs (dense
+      // products in the reference's float order) would overflow the buckets:
+      // they go straight to the sort path.
+      const uint64_t hiK = pb.KH == ~0ull ? pb.kmax + 1 : std::min(pb.KH, pb.kmax + 1);
+      const uint64_t loK = std::max(pb.KL, pb.kmin);
+      const bool dense_like = hiK > loK && hiK - loK <= 4 * total;  // the dense path's criterion
+      const bool bucket = o.path != PGPU_PATH_SORT && !getenv("PGPU_NO_BUCKET") &&
+                          !(ordered && o.path == PGPU_PATH_AUTO && dense_like);
       int nbucket = 0;
       int r = PGPU_OK;
       for (double scale = 1.0; scale >= 0.25; scale *= 0.5) {

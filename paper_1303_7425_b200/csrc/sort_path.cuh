@@ -319,6 +319,7 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
   for (int k = 0; k < kRsIpt; ++k) {
     if (dig[k] != 0xffffffffu) {
       const uint32_t pos = tstart[dig[k]] + wcnt[w][dig[k]] + rank[k];
+      PGPU_ASSERT(pos < (uint32_t)kRsTile);
       skey[pos] = key[k];
       sval[pos] = val[k];
     }
@@ -329,6 +330,7 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
     const KT kk = skey[q];
     const unsigned d = (unsigned)((uint64_t)kk >> shift) & 0xffu;
     const uint64_t g = (uint64_t)gbase[d] + gpre[d] + (q - tstart[d]);
+    PGPU_ASSERT(g < n);
     kout[g] = kk;
     vout[g] = sval[q];
   }

@@ -43,8 +43,13 @@ class MulConfig:
                      reference would use and is validated the same way; both
                      produce identical output (merge.py:1-16), as does the GPU.
     path          -- "auto" | "dense" | "sort" | "bucket" | "small" (device algorithm)
-    float_ordered -- fold float coefficients in the reference's row order so
-                     doubles are bit-identical to the CPU (sort path)
+    float_ordered -- float coefficients: True folds every term in the
+                     reference's row order (merge.py:32-33), so doubles are
+                     bit-identical to the CPU (the dense path is skipped);
+                     False also allows the dense path, whose warp copies fold
+                     a term in a fixed order of its own (run-to-run identical,
+                     within 2k*2^-53*sum|a_i b_j| of the reference); None
+                     (default) means True
     device        -- CUDA ordinal
     """
 
@@ -52,8 +57,24 @@ class MulConfig:
     c: int = 1
     merger: str = "heap"
     path: str = "auto"
-    float_ordered: bool = False
+    float_ordered: bool | None = None
     device: int = 0
+
+    @property
+    def ordered(self) -> bool:
+        return self.float_ordered is None or bool(self.float_ordered)
+
+    @classmethod
+    def of(cls, cfg) -> "MulConfig":
+        """Our config from None, our own, or the reference's MulConfig (l, c,
+        merger; parmul.py:29-43) -- the drop-in receives the reference's."""
+        if cfg is None:
+            return cls()
+        if isinstance(cfg, cls):
+            return cfg
+        return cls(l=getattr(cfg, "l", DEFAULT_GRID_DENSITY), c=getattr(cfg, "c", 1),
+                   merger=getattr(cfg, "merger", "heap"), path=getattr(cfg, "path", "auto"),
+                   float_ordered=getattr(cfg, "float_ordered", None), device=getattr(cfg, "device", 0))
 
     def __post_init__(self):
         if self.l < 1:
@@ -255,12 +276,11 @@ def mul(a, b, cfg: MulConfig | None = None, *, split=None):
 
     Exactly equal to the schoolbook product for int coefficients; for floats
     equal within 2*k*2^-53*sum|a_i b_j| per term (k = products in the term),
-    or bit-identical with cfg.float_ordered.  `split` keeps the reference's
+    and bit-identical by default (cfg.float_ordered None/True).  `split` keeps the reference's
     semantics: products whose exponent is below split.bounds[0] are not formed
     (split.py:44-50 only checks ascent and the sentinel).
     """
-    if cfg is None:
-        cfg = MulConfig()
+    cfg = MulConfig.of(cfg)
     check_compatible(a, b)
     cls = type(a)
     if a.is_zero or b.is_zero:
@@ -270,7 +290,7 @@ def mul(a, b, cfg: MulConfig | None = None, *, split=None):
     if split is not None:
         lo = int(split.bounds[0])
     raw = native_mul(Operand.from_poly(a), Operand.from_poly(b), a.layout, lo=lo,
-                     path=cfg.path, float_ordered=cfg.float_ordered, device=cfg.device)
+                     path=cfg.path, float_ordered=cfg.ordered, device=cfg.device)
     return to_poly(cls, a.layout, a.ctype, raw)
 
 
@@ -279,15 +299,14 @@ def mul_arrays(a, b, cfg: MulConfig | None = None, *, split=None):
     the C ABI returns; Python lists are built only if
     asked for.  Operands may be Polynomial or ArrayPolynomial."""
     from .arrays import ArrayPolynomial
-    if cfg is None:
-        cfg = MulConfig()
+    cfg = MulConfig.of(cfg)
     check_compatible(a, b)
     if a.is_zero or b.is_zero:
         return ArrayPolynomial.zero(a.layout, a.ctype)
     check_product_fits(a, b)
     lo = 0 if split is None else int(split.bounds[0])
     raw = native_mul(Operand.from_poly(a), Operand.from_poly(b), a.layout, lo=lo,
-                     path=cfg.path, float_ordered=cfg.float_ordered, device=cfg.device)
+                     path=cfg.path, float_ordered=cfg.ordered, device=cfg.device)
     return ArrayPolynomial.from_raw(a.layout, a.ctype, raw)
 
 

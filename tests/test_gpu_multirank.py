@@ -42,6 +42,22 @@ def test_emulated_ranks_reproduce_reference_digest(ranks, config, gather):
     assert v["ok"], v
 
 
+def test_bench_self_launches_ranks_without_torchrun():
+    """`bench.py --gpus 3` with no torchrun: it launches the 3 ranks itself (one
+    process per GPU; emulated over gloo when fewer devices are visible), and
+    rank 0 prints one line with n_gpus 3, e2e and the verified product."""
+    cmd = [sys.executable, str(ROOT / "bench.py"), "--gpus", "3", "--config", "fateman20", "--steps", "1",
+           "--warmup", "1", "--verify", "--no-cpu-baseline"]
+    out = subprocess.run(cmd, capture_output=True, text=True, timeout=600, cwd=ROOT)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [json.loads(l) for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    v = lines[0]
+    assert v["n_gpus"] == 3 and v["verified"]["ok"], v.get("verified")
+    assert v["e2e"]["value"] > 0 and v["e2e"]["d2h_bytes_per_step"] > 0
+    assert "gather_ms" in v["multi_gpu"] and "gather" in v["roofline"]["phases_ms"]
+
+
 @pytest.mark.parametrize("ranks,cfg", [(2, "fateman10/int"), (3, "mp12/int"), (2, "fateman10/float")])
 def test_gpu_mul_api_peer_gather(ranks, cfg):
     """cluster.gpu_mul (the multi-GPU public API) over emulated ranks: range

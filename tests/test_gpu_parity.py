@@ -75,7 +75,7 @@ def test_float_ordered_mode_is_bit_exact(cfg):
 @pytest.mark.parametrize("name", ["fateman20", "fateman30", "mp12"])
 def test_float_fast_mode_within_bound(name):
     f, g = benchpolys.CONFIGS[name](float)
-    fast = mul(f, g, MulConfig(path="auto"))
+    fast = mul(f, g, MulConfig(path="auto", float_ordered=False))
     exact = mul(f, g, MulConfig(float_ordered=True))
     assert fast.exps == exact.exps
     # all-positive operands: sum|a_i b_j| == the coefficient itself.  k is the
@@ -104,7 +104,7 @@ def test_float_fast_mode_is_deterministic(name, path):
     f, g = benchpolys.CONFIGS[name](float)
     if path == "small":
         f, g = benchpolys.fateman(2, float)
-    runs = [mul_arrays(f, g, MulConfig(path=path)) for _ in range(3)]
+    runs = [mul_arrays(f, g, MulConfig(path=path, float_ordered=False)) for _ in range(3)]
     e0 = runs[0].exps_array()
     c0 = runs[0].coef_array().view(np.uint64)
     for r in runs[1:]:
@@ -112,12 +112,26 @@ def test_float_fast_mode_is_deterministic(name, path):
         assert np.array_equal(r.coef_array().view(np.uint64), c0)
 
 
-def test_mp12_float_auto_equals_reference_digest():
+@pytest.mark.parametrize("ordered", [None, False])
+def test_mp12_float_auto_equals_reference_digest(ordered):
     """Sparse products fold each term in increasing row (the bucket path's
-    owner fold), so the default float mode is the reference's result bit for bit."""
+    owner fold): the default mode, and the fast mode too, give the
+    reference's result bit for bit on the bucket path."""
+    from paper_1303_7425_b200.parmul import Operand, native_mul
     f, g = benchpolys.CONFIGS["mp12"](float)
-    p = mul(f, g)
+    p = mul(f, g, MulConfig(float_ordered=ordered))
     want = digests()["products"]["mp12/float"]
+    assert p.n == want["n"] and io.poly_digest(p) == want["sha256"]
+    raw = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, float_ordered=bool(ordered))
+    assert raw.path == "bucket"
+
+
+def test_default_float_mode_is_the_reference_order():
+    """mul() without a config (the drop-in call) reproduces the reference's
+    float digests: dense-shaped products skip the dense path."""
+    f, g = benchpolys.CONFIGS["fateman20"](float)
+    p = mul(f, g)
+    want = digests()["products"]["fateman20/float"]
     assert p.n == want["n"] and io.poly_digest(p) == want["sha256"]
 
 
@@ -257,7 +271,7 @@ def test_dense_float_matches_oracle_within_bound(rng):
                     for _ in range(300)], float)
         b = P(lay, [(rng.uniform(-5, 5), (rng.randint(0, 9), rng.randint(0, 9), rng.randint(0, 9)))
                     for _ in range(300)], float)
-        got = mul(a, b, MulConfig(path="dense"))
+        got = mul(a, b, MulConfig(path="dense", float_ordered=False))
         want = O.mul(a, b)
         absa = P._from_sorted(lay, a.exps, [abs(c) for c in a.coeffs], float)
         absb = P._from_sorted(lay, b.exps, [abs(c) for c in b.coeffs], float)
