@@ -248,7 +248,7 @@ __device__ __forceinline__ uint64_t interval_bound(const KT* okey, uint32_t t, u
 constexpr int kNumWarps = PGPU_NUM_WARPS;
 constexpr int kNumThreads = kNumWarps * 32;
 constexpr uint32_t kTbl = 8192;      // keys covered by the shared-memory slot table
-constexpr int kCursorRun = 16;       // rows per thread in the cursor initialisation
+constexpr int kCursorRun = 8;        // rows per thread in the cursor initialisation
 #ifndef PGPU_ACC_KB
 #define PGPU_ACC_KB 80
 #endif
@@ -299,6 +299,7 @@ struct NumArgs {
   uint64_t* ocoef;
   uint32_t* onz;
   uint32_t* unit_ctr;  // persistent CTAs: next unit to claim (zeroed before launch)
+  const uint32_t* act;  // [T][2]: rows [act_lo, act_hi) that can meet interval t (k_active_rows)
 };
 
 // Finished term: NW words -> nl sign-extended u64 limbs + nonzero flag.
@@ -366,10 +367,41 @@ __device__ __forceinline__ void add_unsigned128(uint32_t* a, uint8_t* carry, uin
   if (cy) *carry += 1;
 }
 
+#ifndef PGPU_MAD_CHAIN
+#define PGPU_MAD_CHAIN 1
+#endif
+
 #ifndef PGPU_FOLD_ZERO
 #define PGPU_FOLD_ZERO 0
 #endif
 constexpr bool kFoldZero = PGPU_FOLD_ZERO;
+
+// Ballot of a warp that is converged by construction (every call site runs
+// with all 32 lanes): the raw vote avoids the divergence check and branch
+// the intrinsic adds inside the hot loop.
+__device__ __forceinline__ uint32_t warp_ballot(bool p) {
+  uint32_t r;
+  asm volatile("{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %1, 0;\n\tvote.sync.ballot.b32 %0, q, 0xffffffff;\n\t}"
+               : "=r"(r) : "r"((uint32_t)p));
+  return r;
+}
+
+// Profiling build (-DPGPU_NPROF=1): CTA cycles per phase of k_numeric (thread
+// 0, barrier to barrier) and row-visit / step / pair counts.
+#ifndef PGPU_NPROF
+#define PGPU_NPROF 0
+#endif
+#if PGPU_NPROF
+__device__ unsigned long long g_nprof[8];
+#define NPROF_T(k)                                        \
+  if (threadIdx.x == 0) {                                 \
+    const long long now_ = clock64();                     \
+    atomicAdd(&g_nprof[k], (unsigned long long)(now_ - tprev)); \
+    tprev = now_;                                         \
+  }
+#else
+#define NPROF_T(k)
+#endif
 
 template <typename KT>
 __device__ __forceinline__ uint32_t rank_of(uint64_t klocal, const uint32_t* __restrict__ bits,
@@ -409,7 +441,14 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const uint32_t nb = A.nb;
   if (t_begin >= t_end) return;
-  {  // cursors at the segment's first bound: binary search, then walk left
+#if PGPU_NPROF
+  long long tprev = clock64();
+  unsigned long long visits = 0, steps = 0, npairs = 0;
+#endif
+  {  // cursors at the segment's first bound: binary search for a run's first
+     // row, then a galloping search back from the previous row's cursor (the
+     // count is non-increasing in i; consecutive rows of a degree layer can
+     // differ by thousands of columns, so a linear walk is not bounded)
     const uint64_t K0 = interval_bound(okey, t_begin, A.T, D, A.R1);
     const uint32_t nrow = rb1 - rb0;
     for (uint32_t ch = threadIdx.x; ch * kCursorRun < nrow; ch += blockDim.x) {
@@ -417,22 +456,40 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
       uint32_t c = count_below(bk, nb, (uint64_t)ak[i0], K0);
       for (uint32_t i = i0; i < i1; ++i) {
         uint64_t ai = ak[i];
-        if (i > i0)
-          while (c > 0 && ai + (uint64_t)bk[c - 1] >= K0) --c;
+        if (i > i0 && c > 0 && ai + (uint64_t)bk[c - 1] >= K0) {
+          // the count lies in [0, c - 1]: gallop down, then bisect the bracket
+          uint32_t hi = c - 1, step = 1;
+          while (hi >= step && ai + (uint64_t)bk[hi - step] >= K0) {
+            hi -= step;
+            step <<= 1;
+          }
+          uint32_t lo = hi >= step ? hi - step + 1 : 0;  // P(lo - 1) holds (or lo = 0)
+          while (lo < hi) {  // first j in [lo, hi] with ai + bk[j] >= K0 (hi qualifies)
+            const uint32_t mid = (lo + hi) >> 1;
+            if (ai + (uint64_t)bk[mid] < K0) lo = mid + 1; else hi = mid;
+          }
+          c = lo;
+        }
+        PGPU_ASSERT(c == count_below(bk, nb, ai, K0));
         cur[i] = c;
         nk[i] = c < nb ? (KT)(ai + (uint64_t)bk[c]) : kInf;
       }
     }
   }
   __syncthreads();
+  NPROF_T(0)
   for (uint32_t t = t_begin; t < t_end; ++t) {
     const uint64_t Klo = interval_bound(okey, t, A.T, D, A.R1);
     const uint64_t Khi = interval_bound(okey, t + 1, A.T, D, A.R1);
     const KT kmax = (KT)(Khi - 1);  // keys of the interval: [Klo, kmax]
     const uint32_t base = t * D;
+    // rows that can meet the interval: a_i + b_0 < Khi (started) and
+    // a_i + b_last >= Klo (not finished); a is ascending, so a contiguous span
+    const uint32_t act_lo = max(rb0, __ldg(A.act + 2 * t)), act_hi = min(rb1, __ldg(A.act + 2 * t + 1));
+    const uint32_t g_first = act_lo > rb0 ? (act_lo - rb0) & ~31u : 0u;  // 32-row groups from rb0
     const uint32_t dcount = min(D, A.nout - base);
     const bool use_tbl = (Khi - Klo) <= kTbl;
-    if (threadIdx.x == 0) row_ctr = 0;
+    if (threadIdx.x == 0) row_ctr = g_first;
     // the fold zeroes the copies it reads, so only a unit's first interval clears
     if (!kFoldZero || t == t_begin)
       for (uint32_t k = threadIdx.x; k < G::tbl_off / 4; k += blockDim.x) acc[k] = 0;
@@ -462,7 +519,8 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
     auto step = [&](const KT akr, const uint64_t a0, const double ad, const uint32_t ri,
                     const uint32_t c, auto tbl_mode) -> uint32_t {
       constexpr bool TBL = decltype(tbl_mode)::value;
-      const KT* __restrict__ bkr = bk + c + lane;  // row-relative: immediate offsets per u
+      const uint32_t cl = c + lane;                // 32-bit column index: 2-instruction addresses
+      const KT* __restrict__ bkr = bk + cl;        // row-relative: immediate offsets per u
       uint32_t nv = 0;
       uint32_t slot[kUnroll];
       bool okk[kUnroll];
@@ -482,7 +540,7 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
           ok = j < nb && dk <= span_t;
           off = (uint32_t)dk;
         }
-        nv += __popc(__ballot_sync(0xffffffffu, ok));
+        nv += __popc(warp_ballot(ok));
         uint32_t sl;
         if constexpr (TBL) {
           sl = tbl[min(off, kTbl - 1)];
@@ -494,25 +552,49 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
         okk[u] = ok;
       }
       if constexpr (MODE == 1 && CB) {
-        const long long* __restrict__ bcr = reinterpret_cast<const long long*>(A.bc) + c + lane;
+        const long long* __restrict__ bcr = reinterpret_cast<const long long*>(A.bc) + cl;
         const uint32_t al = (uint32_t)a0, ah = (uint32_t)(a0 >> 32);
         uint64_t* p64 = reinterpret_cast<uint64_t*>(acc) + 2 * w * DP;
 #pragma unroll
         for (int u = 0; u < kUnroll; ++u) {
           const uint64_t b0 = okk[u] ? (uint64_t)__ldg(bcr + 32 * u) : 0ull;
           const uint32_t bl = (uint32_t)b0, bh = (uint32_t)(b0 >> 32);
+          // one 16-byte element (4 words) per (warp, term): a single LDS.128/STS.128
+          uint4* e = reinterpret_cast<uint4*>(p64) + slot[u];
+          uint4 v = *e;
+#if PGPU_MAD_CHAIN
+          // acc += a*b as three multiply-add carry chains over the 32-bit words
+          // (al*bl, ah*bh; al*bh << 32; ah*bl << 32); cy counts the wrap of
+          // the 128-bit element (at most one: the product is below 2^128)
+          uint32_t cy;
+          asm("mad.lo.cc.u32  %0, %5, %7, %0;\n\t"
+              "madc.hi.cc.u32 %1, %5, %7, %1;\n\t"
+              "madc.lo.cc.u32 %2, %6, %8, %2;\n\t"
+              "madc.hi.cc.u32 %3, %6, %8, %3;\n\t"
+              "addc.u32       %4, 0, 0;\n\t"
+              "mad.lo.cc.u32  %1, %5, %8, %1;\n\t"
+              "madc.hi.cc.u32 %2, %5, %8, %2;\n\t"
+              "addc.cc.u32    %3, %3, 0;\n\t"
+              "addc.u32       %4, %4, 0;\n\t"
+              "mad.lo.cc.u32  %1, %6, %7, %1;\n\t"
+              "madc.hi.cc.u32 %2, %6, %7, %2;\n\t"
+              "addc.cc.u32    %3, %3, 0;\n\t"
+              "addc.u32       %4, %4, 0;"
+              : "+r"(v.x), "+r"(v.y), "+r"(v.z), "+r"(v.w), "=r"(cy)
+              : "r"(al), "r"(ah), "r"(bl), "r"(bh));
+#else
           // 64x64 -> 128 from four 32x32 -> 64 partial products
           const uint64_t t0 = (uint64_t)al * bl;
           const uint64_t t1 = (uint64_t)al * bh + (t0 >> 32);
           const uint64_t t2 = (uint64_t)ah * bl + (uint32_t)t1;
           const uint64_t t3 = (uint64_t)ah * bh + (t1 >> 32) + (t2 >> 32);
           const uint64_t lo = (t2 << 32) | (uint32_t)t0;
-          // one 16-byte element {lo, hi} per (warp, term): a single LDS.128/STS.128
-          ulonglong2* e = reinterpret_cast<ulonglong2*>(p64) + slot[u];
-          ulonglong2 v = *e;
+          uint64_t vx = ((uint64_t)v.y << 32) | v.x, vy = ((uint64_t)v.w << 32) | v.z;
           uint32_t cy;
           asm("add.cc.u64 %0, %0, %3;\n\taddc.cc.u64 %1, %1, %4;\n\taddc.u32 %2, 0, 0;"
-              : "+l"(v.x), "+l"(v.y), "=r"(cy) : "l"(lo), "l"(t3));
+              : "+l"(vx), "+l"(vy), "=r"(cy) : "l"(lo), "l"(t3));
+          v = make_uint4((uint32_t)vx, (uint32_t)(vx >> 32), (uint32_t)vy, (uint32_t)(vy >> 32));
+#endif
           *e = v;
           if (cy) cbyte[w * DP + slot[u]] += 1;
         }
@@ -565,13 +647,13 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
       for (uint32_t it = 0;; ++it) {
         uint32_t g;
         if constexpr (MODE == 0) {
-          g = rb0 + (w + it * kNumWarps) * kRowClaim;
+          g = rb0 + g_first + (w + it * kNumWarps) * kRowClaim;
         } else {
           g = 0;
           if (lane == 0) g = atomicAdd(&row_ctr, (uint32_t)kRowClaim);
           g = rb0 + __shfl_sync(0xffffffffu, g, 0);
         }
-        if (g >= rb1) break;
+        if (g >= act_hi) break;
         const uint32_t i = g + lane;
         const bool rowok = lane < kRowClaim && i < rb1;
         uint32_t ci = rowok ? cur[i] : 0u;
@@ -593,8 +675,15 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
           for (;;) {
             const uint32_t nv = step(akr, a0, ad, g + src, c, tbl_mode);
             c += nv;
+#if PGPU_NPROF
+            ++steps;
+            npairs += nv;
+#endif
             if (nv < 32u * kUnroll) break;
           }
+#if PGPU_NPROF
+          ++visits;
+#endif
 #if PGPU_ROW_SELECT
           // branch-free: every lane computes, the row's owner keeps it
           const KT nxt = c < nb ? (KT)(akr + __ldg(bk + (c < nb ? c : 0))) : kInf;
@@ -614,9 +703,11 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
         }
       }
     };
+    NPROF_T(1)
     if (use_tbl) rows(std::integral_constant<bool, true>{});
     else rows(std::integral_constant<bool, false>{});
     __syncthreads();
+    NPROF_T(2)
     // one owner thread per output slot folds the warps' private copies
     for (uint32_t sl = threadIdx.x; sl < dcount; sl += blockDim.x) {
       const uint32_t o = base + sl;
@@ -687,7 +778,15 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
     // with kFoldZero the next interval's table build needs no barrier here: the
     // barrier after it orders this fold before the next interval's rows
     if (!kFoldZero) __syncthreads();
+    NPROF_T(3)
   }
+#if PGPU_NPROF
+  if (lane == 0) {
+    atomicAdd(&g_nprof[4], visits);
+    atomicAdd(&g_nprof[5], steps);
+    atomicAdd(&g_nprof[6], npairs);
+  }
+#endif
 }
 
 // Persistent CTAs (one per resident slot) claim (row block, segment) units in
@@ -712,6 +811,20 @@ k_numeric(NumArgs A) {
 #else
   numeric_unit<KT, NW, MODE, CB>(A, blockIdx.x);
 #endif
+}
+
+// Active row span of every interval t: rows [lo, hi) whose run can meet
+// [bound_t, bound_t+1) -- finished rows (a_i + b_last < Klo) and rows not
+// yet started (a_i + b_0 >= Khi) are skipped by the numeric pass.
+template <typename KT>
+__global__ void __launch_bounds__(256)
+k_active_rows(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk, uint32_t nb,
+              const KT* __restrict__ okey, uint32_t T, uint32_t D, uint64_t R1, uint32_t* __restrict__ act) {
+  const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint64_t Klo = interval_bound(okey, t, T, D, R1), Khi = interval_bound(okey, t + 1, T, D, R1);
+  act[2 * t] = count_below(ak, na, (uint64_t)bk[nb - 1], Klo);
+  act[2 * t + 1] = count_below(ak, na, (uint64_t)bk[0], Khi);
 }
 
 // ---- D5 ---------------------------------------------------------------------

@@ -20,6 +20,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <ctime>
 #include <map>
 #include <mutex>
 #include <set>
@@ -302,6 +303,33 @@ void free_device_ptr(void* p, void* owner) {
   cudaFreeAsync(p, 0);
 }
 
+// Host timeline of one call (PGPU_TRACE=1): where the wall time of a product
+// goes between launches and synchronisations.
+struct Trace {
+  bool on = false;
+  int n = 0;
+  const char* what[32];
+  double t[32];
+  static double now() {
+    timespec ts;
+    clock_gettime(CLOCK_MONOTONIC, &ts);
+    return ts.tv_sec * 1e3 + ts.tv_nsec * 1e-6;
+  }
+  void at(const char* w) {
+    if (on && n < 32) {
+      what[n] = w;
+      t[n++] = now();
+    }
+  }
+  void dump() {
+    if (!on || n < 2) return;
+    fprintf(stderr, "[pgpu trace]");
+    for (int k = 1; k < n; ++k) fprintf(stderr, " %s=%.3f", what[k], t[k] - t[k - 1]);
+    fprintf(stderr, " total=%.3f ms\n", t[n - 1] - t[0]);
+  }
+};
+thread_local Trace g_trace;
+
 struct Timer {
   bool on = false;
   cudaStream_t st;
@@ -576,7 +604,9 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   std::vector<double> hsum(ga + gb);
   CUDA_TRY(cudaMemcpyAsync(&hs, dst, sizeof hs, cudaMemcpyDeviceToHost, ctx.st));
   CUDA_TRY(cudaMemcpyAsync(hsum.data(), dsum, 8ull * (ga + gb), cudaMemcpyDeviceToHost, ctx.st));
+  g_trace.at("stats_launch");
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  g_trace.at("stats_sync");
   // rigorous upper bounds of sum|a_i| and sum|b_j|: device partials are rounded
   // up; the host sum gets the recursive-summation error margin on top
   double sa = 0, sb = 0;
@@ -695,7 +725,9 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   unsigned long long thr[6];
   CUDA_TRY(cudaMemcpyAsync(thr, dthr, 16, cudaMemcpyDeviceToHost, ctx.st));
   CUDA_TRY(cudaMemcpyAsync(thr + 2, dends, 32, cudaMemcpyDeviceToHost, ctx.st));
+  g_trace.at("thresholds_launch");
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  g_trace.at("thresholds_sync");
   if (need[0]) pb.KL = thr[0];  // ~0 when no pair reaches lo: empty range
   if (need[1]) pb.KH = thr[1];  // ~0 when every pair is below hi
   pb.kmin = thr[2] + thr[4];
@@ -767,6 +799,12 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   if (o.lo >= o.hi) return fail(PGPU_EINVAL, "empty exponent range");
   if (a->n == 0 || b->n == 0) return PGPU_OK;  // Polynomial.zero (parmul.py:102-103)
 
+  g_trace.on = getenv("PGPU_TRACE") != nullptr;
+  g_trace.n = 0;
+  g_trace.at("entry");
+  struct TraceDump {
+    ~TraceDump() { g_trace.dump(); }
+  } trace_dump;
   cudaStream_t lib_st;
   TRY(device_setup(o.device, &lib_st));
   Ctx ctx;
@@ -913,7 +951,9 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
       at += s.n;
     }
   }
+  g_trace.at("output_launch");
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  g_trace.at("output_sync");
   ctx.tm.mark(5, "output");
   ctx.tm.finish(out);
   CUDA_TRY(cudaGetLastError());
