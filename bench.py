@@ -60,6 +60,8 @@ def parse():
                     help="device algorithm: auto | dense | bucket | sort | small (pgpu_options.path)")
     ap.add_argument("--gather", default="peer", choices=("peer", "collective"),
                     help="N>1: assemble the slices by peer copies (CUDA IPC) or an all-gather")
+    ap.add_argument("--rebalance", type=int, default=2,
+                    help="N>1: rounds of cost rebalancing of the partition during warm-up")
     ap.add_argument("--flush-mib", type=int, default=512)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -458,6 +460,41 @@ def main():
         if r is not None:
             r.free()
     torch.cuda.synchronize()
+    rebalanced = 0
+    if world > 1 and args.rebalance > 0:
+        # cost balancing (part of the plan): every rank times its own range
+        # product, the times are all-gathered, and the intervals are re-cut
+        # by partition_by_ops on the measured cost density (cluster.rebalance)
+        from paper_1303_7425_b200.cluster import rebalance
+        for _ in range(args.rebalance):
+            ts = []
+            for _ in range(3):
+                flush.zero_()
+                e0 = torch.cuda.Event(enable_timing=True)
+                e1 = torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                r = range_product(dA, dB)
+                e1.record(stream)
+                e1.synchronize()
+                ts.append(e0.elapsed_time(e1))
+                if r is not None:
+                    r.free()
+            mine = torch.tensor([statistics.median(ts)], dtype=torch.float64)
+            allt = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
+            if args.emulate_ranks:
+                dist.all_gather(allt, mine)
+            else:
+                allt = [x.to(dev) for x in allt]
+                dist.all_gather(allt, mine.to(dev))
+            plan = rebalance(plan, [float(x.item()) for x in allt])
+            lo, hi = plan.range_of(rank)
+            my_pairs[0] = 0
+            rebalanced += 1
+        for _ in range(2):  # warm the new ranges (pair counts, workspace)
+            r = step()
+            if r is not None:
+                r.free()
+        torch.cuda.synchronize()
 
     clocks = {"nvml": NvmlClocks, "nvidia-smi": Clocks}.get(args.clock_sampler, lambda i: None)(local)
     if world > 1:
@@ -542,11 +579,17 @@ def main():
         b_alg_step = 32 * total_pairs + (8 + w_c) * n_all + (8 + w_in) * (f.n + g.n)
         kern_pairs = total_pairs / world
         achieved = 32 * kern_pairs / (kern_ms / 1e3) / 1e9 if kern else None
-        traffic = None
-        prof = ROOT / "profiles" / "numeric_dram_bytes.json"
-        if prof.exists():
+        kfam = {"numeric": "k_numeric", "bucket_reduce": "k_bucket_reduce", "reduce": "k_seg_reduce",
+                "sort": "k_rs_onesweep"}.get(kern)
+        traffic, traffic_src = None, None
+        prof = ROOT / "profiles" / "dram_bytes.json"
+        if prof.exists() and kfam:  # ncu-measured DRAM bytes of the kernel over one product
             try:
-                traffic = json.loads(prof.read_text()).get(args.config, {}).get("dram_bytes_per_launch")
+                rec = json.loads(prof.read_text()).get(f"{args.config}/{args.coeff}", {})
+                hit = {k: v for k, v in rec.get("kernels", {}).items() if k.startswith(kfam)}
+                if hit and world == 1:
+                    traffic = sum(v["dram_bytes"] for v in hit.values())
+                    traffic_src = rec.get("source")
             except Exception:
                 traffic = None
         kname = {"numeric": f"k_numeric ({path_used} path)",
@@ -555,12 +598,30 @@ def main():
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,
+                "traffic_source": traffic_src,
                 "peak_source": peak_src, "kernel_ms": kern_ms,
                 "algorithmic_bytes": "32 B per term product (SURVEY.md 8d: one 16-B pair record "
-                                     "written + read); the fused kernel never materialises pairs, "
-                                     "so frac > 1 means it moves less than the modelled pipeline",
+                                     "written + read) over the kernel's time; the fused dense kernel "
+                                     "never materialises pairs, so frac > 1 means it moves less than "
+                                     "the modelled pipeline",
                 "step_frac": b_alg_step / (ms_per_step / 1e3) / 1e9 / (peak * world),
                 "phases_ms": phases}
+        if kern == "numeric":
+            # the dense kernel's real limiter is the shared-memory / L1 pipe:
+            # per term product a 16-byte accumulator read-modify-write (32 B)
+            # plus the 2-byte slot-table lookup, against 128 B/clk per SM
+            sm_mhz = (ck or {}).get("sm_mhz") or 1965.0
+            nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+            smem_peak = 128.0 * nsm * sm_mhz * 1e6 / 1e9
+            smem_ach = 34.0 * kern_pairs / (kern_ms / 1e3) / 1e9
+            roof["bound"] = "smem"
+            roof["smem"] = {"achieved": smem_ach, "peak": smem_peak, "unit": "GB/s",
+                            "frac": smem_ach / smem_peak, "bytes_per_pair": 34,
+                            "peak_def": f"128 B/clk x {nsm} SMs x {sm_mhz:.0f} MHz (median SM clock "
+                                        "under load)",
+                            "note": "frac (above) is the SURVEY 8(d) HBM model; the kernel moves "
+                                    "~0.3 GB of DRAM per product (traffic) and is bound by the "
+                                    "shared-memory/L1 pipe"}
         emulated = bool(args.emulate_ranks and world > 1)
         out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
@@ -583,8 +644,9 @@ def main():
                                      "collective": "all-gather of disjoint slices",
                                      "none": "none (1 GPU)"}[gather_kind],
                           "l2": f"flushed ({args.flush_mib} MiB write) between timed steps",
-                          "plan": "select_grid(l=64) + O_k partition (partition_by_ops), and each "
-                                  "range's pair count from the first product: once per operand pair"
+                          "plan": ("select_grid(l=64) + O_k partition (partition_by_ops), "
+                                   f"{rebalanced} round(s) of re-cutting by measured cost, and each range's "
+                                   "pair count from the first product: once per operand pair")
                           if world > 1 else "none (1 GPU)",
                           "plan_ms": plan_ms, "step_ms": [round(x, 3) for x in times]},
                "roofline": roof, "gpu_launches": launches, "clocks": ck}

@@ -126,6 +126,30 @@ def make_plan(a, b, l: int, world: int, rank: int, count_fn, group=None) -> Rank
     return RankPlan(bounds, plan, [rank_range(bounds, plan, r) for r in range(world)], [0] * world)
 
 
+def rebalance(plan: RankPlan, times) -> RankPlan:
+    """Re-cut the intervals by measured cost: partition_by_ops (the reference's
+    greedy cumulative cut, cluster.py:261-280) applied to a cost density in
+    which interval k of rank r weighs O_k * t_r / P_r (t_r the rank's measured
+    product time, P_r its pair count).  Pair counts alone do not balance the
+    device work: a range of low-degree terms has short row runs and more row
+    visits per pair."""
+    op = plan.plan.op_counts
+    w = [0.0] * len(op)
+    for r, (l1, l2) in enumerate(plan.plan.ranges):
+        pr = sum(op[l1:l2])
+        if pr == 0:
+            continue
+        for k in range(l1, l2):
+            w[k] = op[k] * float(times[r]) / pr
+    tot = sum(w)
+    if tot <= 0:
+        return plan
+    iw = [int(round(x * (1e12 / tot))) for x in w]
+    cut = partition_by_ops(iw, plan.n)
+    new = ClusterPlan(plan.n, cut.ranges, plan.plan.op_counts)
+    return RankPlan(plan.bounds, new, [rank_range(plan.bounds, new, r) for r in range(plan.n)], [0] * plan.n)
+
+
 def plan_all_ranks(a, b, l: int, n: int, count_fn) -> RankPlan:
     """The N-rank plan computed by one process (every block's O_k on this
     GPU): the virtual-rank mode, where one GPU runs the N range products one

@@ -46,7 +46,7 @@ struct KeyPlan {
   uint64_t cmask[kMaxFields]; // compact-field mask
 };
 
-__device__ __forceinline__ uint64_t compact_word(uint64_t e, const KeyPlan& P) {
+__host__ __device__ __forceinline__ uint64_t compact_word(uint64_t e, const KeyPlan& P) {
   uint64_t k = 0;
 #pragma unroll 1
   for (int f = 0; f < P.nf; ++f)

@@ -64,6 +64,7 @@ constexpr int kSymCols = 256;
 #define PGPU_SYM_WIN 49152
 #endif
 constexpr uint32_t kSymWin = PGPU_SYM_WIN;
+constexpr int kSymMaxRowTiles = 512;  // row tiles listed in shared memory (else all tiles visited)
 
 #ifndef PGPU_SYM_SWZ
 #define PGPU_SYM_SWZ 1
@@ -99,11 +100,60 @@ k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t*
   __shared__ KT sb[kSymCols];
   __shared__ __align__(16) KT sa[kSymRows];
   __shared__ uint32_t slo[kSymRows], shi[kSymRows];
+  __shared__ uint32_t tpre[kSymMaxRowTiles + 1];  // nonempty tiles before row tile rt
+  __shared__ uint16_t tclo[kSymMaxRowTiles];      // first nonempty column tile of row tile rt
+  __shared__ uint32_t tsh[33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
   const uint32_t ntr = (na + trows - 1) / trows, ntc = (nb + kSymCols - 1) / kSymCols;
-  const uint64_t ntiles = (uint64_t)ntr * ntc;
+  uint64_t ntiles = (uint64_t)ntr * ntc;
+  // List only the tiles that meet the key range: a row tile [r0, r1) meets
+  // columns [rlo[r1-1], rhi[r0]) (row windows shrink leftwards with i).  A
+  // product restricted to a narrow range (one rank of the multi-GPU split)
+  // would otherwise visit every tile of the full pair matrix.
+  const bool listed = ntr <= (uint32_t)kSymMaxRowTiles && ntc <= 65536u;
+  if (listed) {
+    constexpr int C = (kSymMaxRowTiles + 255) / 256;
+    uint32_t cnt[C], sum = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const uint32_t rt = threadIdx.x * C + c;
+      cnt[c] = 0;
+      if (rt < ntr) {
+        const uint32_t r0 = rt * trows, r1 = min(r0 + trows, na);
+        const uint32_t lo = rlo[r1 - 1], hi = rhi[r0];
+        if (hi > lo) {
+          cnt[c] = (hi - 1) / kSymCols - lo / kSymCols + 1;
+          tclo[rt] = (uint16_t)(lo / kSymCols);
+        }
+      }
+      sum += cnt[c];
+    }
+    uint32_t tot;
+    uint32_t ex = block_excl_scan(sum, tsh, &tot);
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const uint32_t rt = threadIdx.x * C + c;
+      if (rt < ntr) tpre[rt] = ex;
+      ex += cnt[c];
+    }
+    if (threadIdx.x == 0) tpre[ntr] = tot;
+    __syncthreads();
+    ntiles = tot;
+  }
   for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    const uint32_t tr = (uint32_t)(tile % ntr), tc = (uint32_t)(tile / ntr);
+    uint32_t tr, tc;
+    if (listed) {  // row tile: the last rt with tpre[rt] <= tile
+      uint32_t lo = 0, hi = ntr - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (tpre[mid] <= (uint32_t)tile) lo = mid; else hi = mid - 1;
+      }
+      tr = lo;
+      tc = tclo[tr] + ((uint32_t)tile - tpre[tr]);
+    } else {
+      tr = (uint32_t)(tile % ntr);
+      tc = (uint32_t)(tile / ntr);
+    }
     const uint32_t r0 = tr * trows, r1 = min(r0 + trows, na);
     const uint32_t c0 = tc * kSymCols, c1 = min(c0 + kSymCols, nb);
     // rows' column ranges shrink leftwards with i: the tile is empty unless

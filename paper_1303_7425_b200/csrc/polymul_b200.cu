@@ -85,7 +85,9 @@ struct DeviceState {
                                         // slow and occasionally blocks for milliseconds)
   std::mutex mu;       // one product per device at a time uses the workspace
   uint8_t* stage = nullptr;  // pinned staging for small host operands (copy_in_small)
+  uint8_t* rb = nullptr;     // pinned readback of small device values (counts, statistics)
 };
+constexpr size_t kReadback = 64 << 10;
 std::mutex g_mu;
 DeviceState g_dev[64];
 
@@ -100,6 +102,7 @@ int device_setup(int dev, cudaStream_t* st) {
     uint64_t thr = ~0ull;
     CUDA_TRY(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr));
     CUDA_TRY(cudaMemGetInfo(&d.mem_free0, &d.mem_total));
+    CUDA_TRY(cudaMallocHost((void**)&d.rb, kReadback));
     d.init = true;
   }
   *st = d.stream;
@@ -379,6 +382,18 @@ struct Ctx {
   int64_t launches = 0;
   int sms = 148;
   int device = 0;
+  uint8_t* rb = nullptr;  // pinned readback area of the device (the device lock is held)
+  size_t rb_used = 0;
+  // pinned host slots for small device-to-host reads (a pageable destination
+  // makes cudaMemcpyAsync a staged, synchronous copy: ~50 us each)
+  template <typename T>
+  T* pin(size_t n) {
+    const size_t bytes = (n * sizeof(T) + 15) & ~size_t(15);
+    if (!rb || rb_used + bytes > kReadback) return nullptr;
+    T* p = reinterpret_cast<T*>(rb + rb_used);
+    rb_used += bytes;
+    return p;
+  }
 };
 
 inline int grid_for(int64_t n, int threads, int cap) {
@@ -424,17 +439,20 @@ int range_rows(Ctx& ctx, const Problem& pb, uint64_t KL, uint64_t KH, uint32_t**
                uint32_t** rhi, uint64_t** off, uint64_t* pairs) {
   TRY(ctx.ar->alloc(rlo, pb.na));
   TRY(ctx.ar->alloc(rhi, pb.na));
-  TRY(ctx.ar->alloc(off, pb.na));
-  uint64_t* part;
-  TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
   k_edges<KT><<<grid_for(pb.na, 256, 1 << 30), 256, 0, ctx.st>>>(
       (const KT*)pb.ak, pb.na, (const KT*)pb.bk, pb.nb, KL, KH, *rlo, *rhi);
   LAUNCHED(1);
+  if (!off) return PGPU_OK;  // the dense path needs the row windows only
+  TRY(ctx.ar->alloc(off, pb.na));
+  uint64_t* part;
+  TRY(ctx.ar->alloc(&part, kMaxScanBlocks + 1));
   int g;
   LAUNCHED(device_scan<uint64_t>(pb.na, LenGen{*rlo, *rhi}, OffOut{*off}, part, &g, ctx.st));
   if (pairs) {
-    CUDA_TRY(cudaMemcpyAsync(pairs, part + g, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.st));
+    uint64_t* p = ctx.pin<uint64_t>(1);
+    CUDA_TRY(cudaMemcpyAsync(p ? p : pairs, part + g, sizeof(uint64_t), cudaMemcpyDeviceToHost, ctx.st));
     CUDA_TRY(cudaStreamSynchronize(ctx.st));
+    if (p) *pairs = *p;
   }
   return PGPU_OK;
 }
@@ -457,8 +475,10 @@ int count_at(Ctx& ctx, const Problem& pb, const std::vector<uint64_t>& bounds,
                                                 db + b0, dc + b0);
     LAUNCHED(1);
   }
-  CUDA_TRY(cudaMemcpyAsync(cum.data(), dc, bounds.size() * 8, cudaMemcpyDeviceToHost, ctx.st));
+  uint64_t* p = ctx.pin<uint64_t>(bounds.size());
+  CUDA_TRY(cudaMemcpyAsync(p ? p : cum.data(), dc, bounds.size() * 8, cudaMemcpyDeviceToHost, ctx.st));
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
+  if (p) std::copy(p, p + bounds.size(), cum.begin());
   return PGPU_OK;
 }
 
@@ -560,7 +580,8 @@ int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice
   for (size_t r = 0; r < ranges.size(); ++r) {
     Slice s;
     bool done = false;
-    if (try_bucket) TRY(bucket_range<KT>(ctx, pb, ranges[r].first, ranges[r].second, counts[r], &s, &done));
+    if (try_bucket)
+      TRY(bucket_range<KT>(ctx, pb, ranges[r].first, ranges[r].second, counts[r], &s, &done, ranges.size() == 1));
     if (done) ++*nbucket;
     else TRY(sort_range<KT>(ctx, pb, ranges[r].first, ranges[r].second, counts[r], &s));
     if (s.n) slices.push_back(s);
@@ -600,13 +621,47 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
     k_stats<2><<<gb, 256, 0, ctx.st>>>(pb.bexp, pb.bcoef, pb.nb, P, dst, 1, dsum + ga);
   }
   LAUNCHED(2);
+  // range thresholds (packed) and operand ends ride the same round trip
+  const uint64_t npairs = (uint64_t)pb.na * pb.nb;
+  const bool small_only = o.lo == 0 && o.hi == ~0ull && npairs <= (uint64_t)kSmallPairs &&
+                          !getenv("PGPU_NO_SMALL") && (o.path == PGPU_PATH_AUTO || o.path == PGPU_PATH_SMALL);
+  uint64_t S[2] = {o.lo, o.hi};
+  const bool need_thr[2] = {o.lo != 0, o.hi != ~0ull};
+  unsigned long long* dthr;  // [0,1] thresholds, [2..5] operand ends
+  TRY(ctx.ar->alloc(&dthr, 6));
+  if (!small_only) {
+    CUDA_TRY(cudaMemsetAsync(dthr, 0xff, 16, ctx.st));  // ~0: no pair reaches the bound
+    for (int sdx = 0; sdx < 2; ++sdx) {
+      if (!need_thr[sdx]) continue;
+      k_threshold<<<grid_for(pb.na, 256, 1 << 30), 256, 0, ctx.st>>>(pb.aexp, pb.na, pb.bexp, pb.nb, S[sdx],
+                                                                      dthr + sdx);
+      LAUNCHED(1);
+    }
+    k_exp_ends<<<1, 32, 0, ctx.st>>>(pb.aexp, pb.na, pb.bexp, pb.nb, dthr + 2);
+    LAUNCHED(1);
+  }
+  g_trace.at("stats_kernels");
   OperandStats hs;
   std::vector<double> hsum(ga + gb);
-  CUDA_TRY(cudaMemcpyAsync(&hs, dst, sizeof hs, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaMemcpyAsync(hsum.data(), dsum, 8ull * (ga + gb), cudaMemcpyDeviceToHost, ctx.st));
+  OperandStats* hs_p = ctx.pin<OperandStats>(1);
+  double* hsum_p = ctx.pin<double>(ga + gb);
+  if (!hs_p || !hsum_p) {
+    hs_p = &hs;
+    hsum_p = hsum.data();
+  }
+  CUDA_TRY(cudaMemcpyAsync(hs_p, dst, sizeof hs, cudaMemcpyDeviceToHost, ctx.st));
+  CUDA_TRY(cudaMemcpyAsync(hsum_p, dsum, 8ull * (ga + gb), cudaMemcpyDeviceToHost, ctx.st));
+  unsigned long long thr_local[6];
+  unsigned long long* thr = ctx.pin<unsigned long long>(6);
+  if (!thr) thr = thr_local;
+  if (!small_only) CUDA_TRY(cudaMemcpyAsync(thr, dthr, 48, cudaMemcpyDeviceToHost, ctx.st));
   g_trace.at("stats_launch");
   CUDA_TRY(cudaStreamSynchronize(ctx.st));
   g_trace.at("stats_sync");
+  if (hs_p != &hs) {
+    hs = *hs_p;
+    std::copy(hsum_p, hsum_p + ga + gb, hsum.begin());
+  }
   // rigorous upper bounds of sum|a_i| and sum|b_j|: device partials are rounded
   // up; the host sum gets the recursive-summation error margin on top
   double sa = 0, sb = 0;
@@ -686,52 +741,24 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
   // packed [lo, hi) -> compact [KL, KH)
   pb.KL = 0;
   pb.KH = ~0ull;
-  const uint64_t npairs = (uint64_t)pb.na * pb.nb;
-  if (o.lo == 0 && o.hi == ~0ull && npairs <= (uint64_t)kSmallPairs &&
-      P.kbits + std::max(1, bitlen64(npairs - 1)) <= 63 && !getenv("PGPU_NO_SMALL") &&
-      (o.path == PGPU_PATH_AUTO || o.path == PGPU_PATH_SMALL)) {
-    // the one-CTA path needs neither thresholds nor key ends: no second round trip
+  if (small_only && P.kbits + std::max(1, bitlen64(npairs - 1)) <= 63) {
+    // the one-CTA path needs neither thresholds nor key ends
     pb.kmin = 0;
     pb.kmax = ~0ull;
     return PGPU_OK;
   }
-  unsigned long long* dthr;
-  TRY(ctx.ar->alloc(&dthr, 2));
-  unsigned long long init[2] = {~0ull, ~0ull};
-  CUDA_TRY(cudaMemcpyAsync(dthr, init, 16, cudaMemcpyHostToDevice, ctx.st));
-  uint64_t S[2] = {o.lo, o.hi};
-  bool need[2] = {o.lo != 0, o.hi != ~0ull};
-  for (int s = 0; s < 2; ++s) {
-    if (!need[s]) continue;
-    int g = grid_for(pb.na, 256, 1 << 30);
-    if (pb.k32)
-      k_threshold<uint32_t><<<g, 256, 0, ctx.st>>>(pb.aexp, (const uint32_t*)pb.ak, pb.na, pb.bexp,
-                                                   (const uint32_t*)pb.bk, pb.nb, S[s], dthr + s);
-    else
-      k_threshold<uint64_t><<<g, 256, 0, ctx.st>>>(pb.aexp, (const uint64_t*)pb.ak, pb.na, pb.bexp,
-                                                   (const uint64_t*)pb.bk, pb.nb, S[s], dthr + s);
+  if (small_only) {  // key too wide for the one-CTA sort word: thresholds after all
+    CUDA_TRY(cudaMemsetAsync(dthr, 0xff, 16, ctx.st));
+    k_exp_ends<<<1, 32, 0, ctx.st>>>(pb.aexp, pb.na, pb.bexp, pb.nb, dthr + 2);
     LAUNCHED(1);
+    CUDA_TRY(cudaMemcpyAsync(thr, dthr, 48, cudaMemcpyDeviceToHost, ctx.st));
+    CUDA_TRY(cudaStreamSynchronize(ctx.st));
   }
-  // key ends (operands are ascending) travel back with the thresholds: one sync
-  unsigned long long* dends;
-  TRY(ctx.ar->alloc(&dends, 4));
-  if (pb.k32)
-    k_key_ends<uint32_t><<<1, 32, 0, ctx.st>>>((const uint32_t*)pb.ak, pb.na, (const uint32_t*)pb.bk,
-                                              pb.nb, dends);
-  else
-    k_key_ends<uint64_t><<<1, 32, 0, ctx.st>>>((const uint64_t*)pb.ak, pb.na, (const uint64_t*)pb.bk,
-                                              pb.nb, dends);
-  LAUNCHED(1);
-  unsigned long long thr[6];
-  CUDA_TRY(cudaMemcpyAsync(thr, dthr, 16, cudaMemcpyDeviceToHost, ctx.st));
-  CUDA_TRY(cudaMemcpyAsync(thr + 2, dends, 32, cudaMemcpyDeviceToHost, ctx.st));
-  g_trace.at("thresholds_launch");
-  CUDA_TRY(cudaStreamSynchronize(ctx.st));
-  g_trace.at("thresholds_sync");
-  if (need[0]) pb.KL = thr[0];  // ~0 when no pair reaches lo: empty range
-  if (need[1]) pb.KH = thr[1];  // ~0 when every pair is below hi
-  pb.kmin = thr[2] + thr[4];
-  pb.kmax = thr[3] + thr[5];
+  // thresholds are packed sums (~0: no pair reaches the bound -> empty range)
+  if (need_thr[0]) pb.KL = thr[0] == ~0ull ? ~0ull : compact_word(thr[0], P);
+  if (need_thr[1]) pb.KH = thr[1] == ~0ull ? ~0ull : compact_word(thr[1], P);
+  pb.kmin = compact_word(thr[2] + thr[4], P);
+  pb.kmax = compact_word(thr[3] + thr[5], P);
   return PGPU_OK;
 }
 
@@ -812,8 +839,11 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
   ctx.device = o.device;
   CUDA_TRY(cudaDeviceGetAttribute(&ctx.sms, cudaDevAttrMultiProcessorCount, o.device));
   DeviceState& dstate = g_dev[o.device & 63];
+  ctx.rb = dstate.rb;
   std::lock_guard<std::mutex> ws_lock(dstate.mu);
+  g_trace.at("setup");
   TRY(grow_workspace(dstate, ctx.st));
+  g_trace.at("workspace");
   Arena ar(ctx.st, &dstate);
   ctx.ar = &ar;
   ctx.mem_budget = dstate.mem_free0 > dstate.ws_cap ? dstate.mem_free0 - dstate.ws_cap : 0;
@@ -833,6 +863,7 @@ int mul_impl(const pgpu_poly* a, const pgpu_poly* b, const pgpu_layout* lay,
     TRY(copy_in(ctx, a, csz, o, &pb.aexp, &pb.acoef));
     TRY(copy_in(ctx, b, csz, o, &pb.bexp, &pb.bcoef));
   }
+  g_trace.at("copy_in");
   TRY(build_problem(ctx, lay, opt, pb, o));
   out->key_bits = pb.P.kbits;
   out->acc_limbs = pb.nl ? pb.nl : 1;

@@ -32,8 +32,9 @@ k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_
   __shared__ unsigned long long smax[kMaxFields];
   __shared__ double ssum[32];
   __shared__ unsigned int sbits, sunsorted, sneg;
+  __shared__ unsigned long long smag;  // max magnitude (nonnegative doubles order as their bits)
   if (threadIdx.x < kMaxFields) smax[threadIdx.x] = 0;
-  if (threadIdx.x == 0) { sbits = 0; sunsorted = 0; sneg = 0; }
+  if (threadIdx.x == 0) { sbits = 0; sunsorted = 0; sneg = 0; smag = 0; }
   __syncthreads();
   unsigned long long lmax[kMaxFields];
 #pragma unroll
@@ -78,17 +79,34 @@ k_stats(const uint64_t* __restrict__ exps, const void* __restrict__ coef, int64_
     }
   }
 #pragma unroll
-  for (int f = 0; f < kMaxFields; ++f)
-    if (f < nf && lmax[f]) atomicMax(&smax[f], lmax[f]);
+  for (int f = 0; f < kMaxFields; ++f) {
+    if (f < nf) {  // warp max first: one shared atomic per warp and field
+      unsigned long long v = lmax[f];
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        const unsigned long long o = __shfl_xor_sync(0xffffffffu, v, d);
+        v = o > v ? o : v;
+      }
+      if ((threadIdx.x & 31) == 0 && v) atomicMax(&smax[f], v);
+    }
+  }
   if (lbits) atomicMax(&sbits, lbits);
   if (lbad) sunsorted = 1;
   if (lneg) sneg = 1;
-  // block sum of the per-thread upper bounds, rounded up
+  // block sum of the per-thread upper bounds (rounded up) and block max of the
+  // magnitudes: one global atomic per block (one per thread serialised on a
+  // single word and cost ~0.1 ms per operand)
 #pragma unroll
-  for (int d = 16; d > 0; d >>= 1) lsum = __dadd_ru(lsum, __shfl_xor_sync(0xffffffffu, lsum, d));
-  if ((threadIdx.x & 31) == 0) ssum[threadIdx.x >> 5] = lsum;
+  for (int d = 16; d > 0; d >>= 1) {
+    lsum = __dadd_ru(lsum, __shfl_xor_sync(0xffffffffu, lsum, d));
+    lmag = fmax(lmag, __shfl_xor_sync(0xffffffffu, lmag, d));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    ssum[threadIdx.x >> 5] = lsum;
+    if (lmag > 0.0) atomicMax(&smag, (unsigned long long)__double_as_longlong(lmag));
+  }
   __syncthreads();
-  if (lmag > 0.0) atomicMax(&st->maxmag[side], (unsigned long long)__double_as_longlong(lmag));
+  if (threadIdx.x == 0 && smag) atomicMax(&st->maxmag[side], smag);
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int q = 0; q < (int)(blockDim.x >> 5); ++q) t = __dadd_ru(t, ssum[q]);
@@ -110,23 +128,40 @@ k_compact(const uint64_t* __restrict__ exps, int64_t n, KeyPlan P, KT* __restric
     out[i] = (KT)compact_word(exps[i], P);
 }
 
-// Smallest compact key of a pair whose packed sum is >= S (ULLONG_MAX if none).
-template <typename KT>
+// Smallest packed sum a_i + b_j >= S (ULLONG_MAX if none).  Compaction is
+// order-preserving and additive on realisable sums, so its compact key is the
+// smallest compact key of a pair at or above S; the host compacts it, which
+// lets the thresholds ride the operand-statistics round trip.
 __global__ void __launch_bounds__(256)
-k_threshold(const uint64_t* __restrict__ aexp, const KT* __restrict__ ak, uint32_t na,
-            const uint64_t* __restrict__ bexp, const KT* __restrict__ bk, uint32_t nb, uint64_t S,
-            unsigned long long* out) {
+k_threshold(const uint64_t* __restrict__ aexp, uint32_t na, const uint64_t* __restrict__ bexp, uint32_t nb,
+            uint64_t S, unsigned long long* out) {
   uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   unsigned long long best = ~0ull;
   if (i < na) {
     uint32_t j = count_below<uint64_t>(bexp, nb, aexp[i], S);
-    if (j < nb) best = (unsigned long long)ak[i] + (unsigned long long)bk[j];
+    if (j < nb) best = (unsigned long long)aexp[i] + (unsigned long long)bexp[j];
   }
   for (int d = 16; d > 0; d >>= 1) {
     unsigned long long o = __shfl_xor_sync(0xffffffffu, best, d);
     best = o < best ? o : best;
   }
-  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(out, best);
+  __shared__ unsigned long long sbest;
+  if (threadIdx.x == 0) sbest = ~0ull;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0 && best != ~0ull) atomicMin(&sbest, best);
+  __syncthreads();
+  if (threadIdx.x == 0 && sbest != ~0ull) atomicMin(out, sbest);
+}
+
+// The smallest and largest packed exponent of each operand.
+__global__ void k_exp_ends(const uint64_t* __restrict__ aexp, uint32_t na, const uint64_t* __restrict__ bexp,
+                           uint32_t nb, unsigned long long* ends) {
+  if (threadIdx.x == 0) {
+    ends[0] = aexp[0];
+    ends[1] = aexp[na - 1];
+    ends[2] = bexp[0];
+    ends[3] = bexp[nb - 1];
+  }
 }
 
 template <typename KT>
@@ -154,17 +189,6 @@ k_count_multi(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk,
 }
 
 // ends[0..3] = ak[0], ak[na-1], bk[0], bk[nb-1] (operands ascending)
-template <typename KT>
-__global__ void k_key_ends(const KT* __restrict__ ak, uint32_t na, const KT* __restrict__ bk,
-                           uint32_t nb, unsigned long long* ends) {
-  if (threadIdx.x == 0) {
-    ends[0] = ak[0];
-    ends[1] = ak[na - 1];
-    ends[2] = bk[0];
-    ends[3] = bk[nb - 1];
-  }
-}
-
 struct LenGen {
   const uint32_t* lo;
   const uint32_t* hi;

@@ -140,6 +140,9 @@ constexpr int kRsWarps = kRsThreads / 32;
 #ifndef PGPU_RS_LOOKBACK
 #define PGPU_RS_LOOKBACK 4
 #endif
+#ifndef PGPU_RS_BACKOFF
+#define PGPU_RS_BACKOFF 1
+#endif
 constexpr int kRsIpt = PGPU_RS_IPT;                // items per thread per tile
 constexpr int kRsTile = kRsThreads * kRsIpt;       // 4096
 constexpr int kRsDigits = 256;
@@ -277,12 +280,14 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
       // kLook predecessors per round trip: the chain of aggregate-only tiles
       // is walked kLook tiles at a time instead of one
       constexpr int kLook = PGPU_RS_LOOKBACK;
+      unsigned backoff = 32;
       for (bool done = false; !done;) {
         unsigned long long v[kLook];
 #pragma unroll
         for (int u = 0; u < kLook; ++u)
           v[u] = k - u >= 0 ? *(volatile unsigned long long*)(status + (uint64_t)(k - u) * kRsDigits + d)
                             : (2ull << 62);  // before tile 0: an inclusive zero
+        bool progress = false;
 #pragma unroll
         for (int u = 0; u < kLook; ++u) {
           if (done) break;
@@ -290,7 +295,14 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
           if (flag == 0) break;  // not published yet: re-poll from here
           excl += v[u] & kValMask;
           --k;
+          progress = true;
           if (flag == kFlagPre) done = true;
+        }
+        // a predecessor still ranking: back off instead of spinning, so the
+        // issue slots go to the SM's other tiles
+        if (!done && !progress && PGPU_RS_BACKOFF) {
+          __nanosleep(backoff);
+          backoff = backoff < 1024 ? backoff * 2 : 1024;
         }
       }
 #else

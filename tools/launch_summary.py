@@ -26,10 +26,23 @@ def main(path, title):
     print(f"# {title}")
     print(f"# one product, ncu launch list (cold-cache, serialised: compare shares, not absolutes)")
     print(f"# step total {tot / 1e6:.3f} ms over {len(sel)} launches")
+    agg = OrderedDict()
     for d in sel:
         t = d.get("gpu__time_duration.sum", 0)
-        print(f"{d['name'][:70]:70s} {t / 1e6:9.3f} ms {100 * t / tot:5.1f}%  dram r {d.get('dram__bytes_read.sum', 0) / 1e6:9.1f} MB"
-              f" w {d.get('dram__bytes_write.sum', 0) / 1e6:9.1f} MB")
+        if len(sel) <= 80:
+            print(f"{d['name'][:70]:70s} {t / 1e6:9.3f} ms {100 * t / tot:5.1f}%  dram r "
+                  f"{d.get('dram__bytes_read.sum', 0) / 1e6:9.1f} MB w {d.get('dram__bytes_write.sum', 0) / 1e6:9.1f} MB")
+        name = d["name"].split("(")[0].replace("void ", "")
+        a = agg.setdefault(name, [0, 0.0, 0.0, 0.0])
+        a[0] += 1
+        a[1] += t
+        a[2] += d.get("dram__bytes_read.sum", 0)
+        a[3] += d.get("dram__bytes_write.sum", 0)
+    print("# per kernel (all launches of the product)")
+    for name, (n, t, r, w) in sorted(agg.items(), key=lambda kv: -kv[1][1]):
+        print(f"{name[:60]:60s} x{n:<4d} {t / 1e6:9.3f} ms {100 * t / tot:5.1f}%  dram {(r + w) / 1e6:10.1f} MB "
+              f"({(r + w) / max(t, 1):8.1f} GB/s)")
+    return agg
 
 
 if __name__ == "__main__":
