@@ -580,7 +580,7 @@ def main():
         kern_pairs = total_pairs / world
         achieved = 32 * kern_pairs / (kern_ms / 1e3) / 1e9 if kern else None
         kfam = {"numeric": "k_numeric", "bucket_reduce": "k_bucket_reduce", "reduce": "k_seg_reduce",
-                "sort": "k_rs_onesweep"}.get(kern)
+                "sort": "k_rs_"}.get(kern)
         traffic, traffic_src = None, None
         prof = ROOT / "profiles" / "dram_bytes.json"
         if prof.exists() and kfam:  # ncu-measured DRAM bytes of the kernel over one product
@@ -594,7 +594,7 @@ def main():
                 traffic = None
         kname = {"numeric": f"k_numeric ({path_used} path)",
                  "bucket_reduce": "k_bucket_reduce (bucket path)", "reduce": "k_seg_reduce (sort path)",
-                 "sort": "k_rs_onesweep passes (sort path)"}.get(kern, kern)
+                 "sort": "radix passes k_rs_count/k_rs_colscan/k_rs_scatter (sort path)"}.get(kern, kern)
         roof = {"bound": "hbm", "kernel": kname,
                 "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": (achieved / peak) if achieved else None, "traffic": traffic,

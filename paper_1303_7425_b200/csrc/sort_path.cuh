@@ -18,6 +18,7 @@
 // k_gen_j writes them, K4 recovers each pair's row from its key through a
 // hash of operand a's keys (k_seg_reduce_*_j).
 #pragma once
+#include <type_traits>
 #include "common.cuh"
 #include "scan.cuh"
 
@@ -345,6 +346,206 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
     PGPU_ASSERT(g < n);
     kout[g] = kk;
     vout[g] = sval[q];
+  }
+}
+
+// ---- K2 (super-tile passes): count / column scan / scatter -------------------
+// The onesweep's decoupled look-back walks every predecessor tile still in
+// flight (~600 on the GPU): on MP n=25 batches its spinning was ~90% of the
+// pass's instructions and the pass ran at ~2 TB/s.  Here a pass is
+//   RS1 k_rs_count    per super-tile (kRsSuper consecutive tiles) digit counts,
+//                     digit-major cnt[d][st]; reads the keys only
+//   RS2 k_rs_colscan  per digit: exclusive scan over the super-tiles (in
+//                     place) and the digit total
+//   RS3 k_rs_scatter  one CTA per super-tile: digit bases from the totals and
+//                     its column prefix, then its tiles in order -- rank each
+//                     tile stably (warp-major, __match_any_sync), stage it in
+//                     shared memory by digit, write each digit's run at the
+//                     running offset.  No inter-CTA waiting at all.
+// Stable like the onesweep: tiles in order inside a super-tile, super-tiles in
+// order through the column prefix, input order inside a tile.
+#ifndef PGPU_RS_SUPER
+#define PGPU_RS_SUPER 8
+#endif
+constexpr int kRsSuper = PGPU_RS_SUPER;
+constexpr uint64_t kRsSuperItems = (uint64_t)kRsSuper * kRsTile;
+
+template <typename KT>
+__global__ void __launch_bounds__(kRsThreads)
+k_rs_count(const KT* __restrict__ keys, uint64_t n, int shift, uint32_t nst, uint32_t* __restrict__ cnt) {
+  __shared__ uint32_t h[kRsDigits];
+  const uint32_t st = blockIdx.x;
+  h[threadIdx.x] = 0;  // kRsThreads == kRsDigits
+  __syncthreads();
+  const uint64_t b0 = (uint64_t)st * kRsSuperItems;
+  const uint64_t b1 = b0 + kRsSuperItems < n ? b0 + kRsSuperItems : n;
+  const unsigned lt = lanemask_lt();
+  // 16-byte loads (V keys per thread per round; b0 is a multiple of V and the
+  // arrays are 256-byte aligned), a uniform trip count for full-warp matches
+  constexpr int V = 16 / sizeof(KT);
+  using Vec = typename std::conditional<sizeof(KT) == 4, uint4, ulonglong2>::type;
+  const Vec* kv = reinterpret_cast<const Vec*>(keys + b0);
+  const uint64_t nv = (b1 - b0 + V - 1) / V;
+#pragma unroll 2
+  for (uint64_t vb = 0; vb < nv; vb += kRsThreads) {
+    const uint64_t vi = vb + threadIdx.x;
+    KT k[V];
+    if (vi < nv && b0 + (vi + 1) * V <= b1) {
+      const Vec x = kv[vi];
+      if constexpr (sizeof(KT) == 4) {
+        k[0] = x.x; k[1] = x.y; k[2] = x.z; k[3] = x.w;
+      } else {
+        k[0] = x.x; k[1] = x.y;
+      }
+    } else {
+#pragma unroll
+      for (int u = 0; u < V; ++u) {
+        const uint64_t i = b0 + vi * V + u;
+        k[u] = (vi < nv && i < b1) ? keys[i] : KT(0);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < V; ++u) {
+      const bool ok = vi < nv && b0 + vi * V + u < b1;
+      const unsigned d = ok ? (unsigned)((uint64_t)k[u] >> shift) & 0xffu : 0x100u;
+      const unsigned peers = __match_any_sync(0xffffffffu, d);
+      if (ok && (peers & lt) == 0) atomicAdd(&h[d], (uint32_t)__popc(peers));
+    }
+  }
+  __syncthreads();
+  cnt[(uint64_t)threadIdx.x * nst + st] = h[threadIdx.x];
+}
+
+// CTA d: exclusive scan of cnt[d][0, nst) in place; tot[d] = the digit's total
+__global__ void __launch_bounds__(1024) k_rs_colscan(uint32_t* __restrict__ cnt, uint32_t nst,
+                                                     uint32_t* __restrict__ tot) {
+  __shared__ uint32_t sh[33];
+  uint32_t* row = cnt + (uint64_t)blockIdx.x * nst;
+  uint32_t carry = 0;
+  constexpr int C = 4;
+  for (uint32_t base = 0; base < nst; base += blockDim.x * C) {
+    const uint32_t i0 = base + threadIdx.x * C;
+    uint32_t v[C], sum = 0;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      v[c] = i0 + c < nst ? row[i0 + c] : 0u;
+      sum += v[c];
+    }
+    uint32_t t;
+    uint32_t ex = block_excl_scan(sum, sh, &t) + carry;
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      if (i0 + c < nst) row[i0 + c] = ex;
+      ex += v[c];
+    }
+    carry += t;
+  }
+  if (threadIdx.x == 0) tot[blockIdx.x] = carry;
+}
+
+#ifndef PGPU_RS_SCAT_MINB
+#define PGPU_RS_SCAT_MINB 2
+#endif
+template <typename KT, typename VT = uint64_t>
+__global__ void __launch_bounds__(kRsThreads, PGPU_RS_SCAT_MINB)
+k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restrict__ kout,
+             VT* __restrict__ vout, uint64_t n, int shift, uint32_t nst, const uint32_t* __restrict__ cnt,
+             const uint32_t* __restrict__ tot) {
+  extern __shared__ __align__(16) uint8_t rs_smem[];
+  VT* sval = reinterpret_cast<VT*>(rs_smem);                         // [kRsTile]
+  KT* skey = reinterpret_cast<KT*>(rs_smem + sizeof(VT) * kRsTile);  // [kRsTile]
+  __shared__ uint32_t wcnt[kRsWarps][kRsDigits];
+  __shared__ uint32_t tstart[kRsDigits];
+  __shared__ uint32_t ttot[kRsDigits];
+  __shared__ unsigned long long run[kRsDigits];  // next output position of each digit
+  __shared__ uint32_t shs[33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const unsigned lt = lanemask_lt();
+  const uint32_t st = blockIdx.x;
+  {  // digit bases: totals of the smaller digits + this super-tile's column prefix
+    const uint32_t d = threadIdx.x;
+    uint32_t t;
+    const uint32_t ex = block_excl_scan(tot[d], shs, &t);
+    run[d] = (unsigned long long)ex + cnt[(uint64_t)d * nst + st];
+  }
+  const uint64_t s0 = (uint64_t)st * kRsSuperItems;
+  // the next tile's items are loaded while this one is ranked and scattered
+  KT key[kRsIpt], nkey[kRsIpt];
+  VT val[kRsIpt], nval[kRsIpt];
+  auto load = [&](uint64_t t0, KT (&kk)[kRsIpt], VT (&vv)[kRsIpt]) {
+    const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
+#pragma unroll
+    for (int k = 0; k < kRsIpt; ++k) {
+      const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
+      const bool ok = idx < end;
+      kk[k] = ok ? kin[idx] : KT(0);
+      vv[k] = ok ? vin[idx] : VT(0);
+    }
+  };
+  if (s0 < n) load(s0, nkey, nval);
+  for (int tl = 0; tl < kRsSuper; ++tl) {
+    const uint64_t t0 = s0 + (uint64_t)tl * kRsTile;
+    if (t0 >= n) break;
+    const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
+#pragma unroll
+    for (int k = 0; k < kRsIpt; ++k) {
+      key[k] = nkey[k];
+      val[k] = nval[k];
+    }
+    if (tl + 1 < kRsSuper && t0 + kRsTile < n) load(t0 + kRsTile, nkey, nval);
+    for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wcnt[0][0])[k] = 0;
+    __syncthreads();
+    uint32_t rank[kRsIpt];
+    unsigned dig[kRsIpt];
+#pragma unroll
+    for (int k = 0; k < kRsIpt; ++k) {
+      const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
+      const bool ok = idx < end;
+      dig[k] = ok ? (unsigned)((uint64_t)key[k] >> shift) & 0xffu : 0u;
+      const unsigned peers = __match_any_sync(0xffffffffu, ok ? dig[k] : 0x100u);
+      const uint32_t c = ok ? wcnt[w][dig[k]] : 0u;
+      __syncwarp();
+      rank[k] = c + __popc(peers & lt);
+      if (ok && (peers & lt) == 0) wcnt[w][dig[k]] = c + __popc(peers);
+      __syncwarp();
+      if (!ok) dig[k] = 0xffffffffu;
+    }
+    __syncthreads();
+    {  // per digit: exclusive over warps and the tile total
+      const int d = threadIdx.x;
+      uint32_t sum = 0;
+#pragma unroll
+      for (int q = 0; q < kRsWarps; ++q) {
+        const uint32_t c = wcnt[q][d];
+        wcnt[q][d] = sum;
+        sum += c;
+      }
+      ttot[d] = sum;
+      uint32_t t;
+      tstart[d] = block_excl_scan(sum, shs, &t);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kRsIpt; ++k) {
+      if (dig[k] != 0xffffffffu) {
+        const uint32_t pos = tstart[dig[k]] + wcnt[w][dig[k]] + rank[k];
+        PGPU_ASSERT(pos < (uint32_t)kRsTile);
+        skey[pos] = key[k];
+        sval[pos] = val[k];
+      }
+    }
+    __syncthreads();
+    const uint32_t tn = (uint32_t)(end - t0);
+    for (uint32_t q = threadIdx.x; q < tn; q += blockDim.x) {
+      const KT kk = skey[q];
+      const unsigned d = (unsigned)((uint64_t)kk >> shift) & 0xffu;
+      const uint64_t g = run[d] + (q - tstart[d]);
+      PGPU_ASSERT(g < n);
+      kout[g] = kk;
+      vout[g] = sval[q];
+    }
+    __syncthreads();
+    run[threadIdx.x] += ttot[threadIdx.x];
   }
 }
 
