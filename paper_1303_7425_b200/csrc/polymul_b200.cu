@@ -373,8 +373,9 @@ struct Timer {
 struct Ctx {
   cudaStream_t st;
   Arena* ar;
-  void* rh_key = nullptr;     // row hash of operand a (sort path j-records: RowSlot<KT>[]), or null
+  void* rh_key = nullptr;     // key/coefficient hash of operand a (sort path j-records: KCSlot[]), or null
   uint32_t rh_mask = 0;
+  void* brec = nullptr;       // operand b as KCSlot[] (j-records)
   uint8_t* batch_blk = nullptr;  // one block reused by every batch of a product
   size_t batch_cap = 0;
   size_t mem_budget = 0;  // bytes this call may plan to use for large scratch
@@ -540,17 +541,26 @@ int run_sort_path(Ctx& ctx, const Problem& pb, uint64_t total, std::vector<Slice
   ctx.rh_key = nullptr;
   const uint64_t jrec_min = getenv("PGPU_JREC_MIN") ? strtoull(getenv("PGPU_JREC_MIN"), nullptr, 10)
                                                    : (1ull << 20);
-  if (total >= jrec_min && pb.P.kbits < (int)(8 * sizeof(KT)) && !getenv("PGPU_NO_JREC")) {
+  if (total >= jrec_min && pb.P.kbits < 64 && !getenv("PGPU_NO_JREC")) {
+    // key/coefficient slots: a hash of operand a, and operand b in order
     uint32_t cap = 1;
     while (cap < 2 * pb.na) cap <<= 1;
-    RowSlot<KT>* slots;
+    KCSlot *slots, *brec;
     TRY(ctx.ar->alloc(&slots, cap));
-    CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(RowSlot<KT>) * cap, ctx.st));
-    k_row_hash_build<KT><<<grid_for(pb.na, 256, 1 << 30), 256, 0, ctx.st>>>((const KT*)pb.ak, pb.na, slots,
-                                                                          cap - 1);
-    LAUNCHED(1);
+    TRY(ctx.ar->alloc(&brec, pb.nb));
+    CUDA_TRY(cudaMemsetAsync(slots, 0xff, sizeof(KCSlot) * cap, ctx.st));
+    const int ga = grid_for(pb.na, 256, 1 << 30), gb = grid_for(pb.nb, 256, 1 << 30);
+    if (pb.ck == PGPU_I128) {
+      k_kc_hash_build<KT, 2><<<ga, 256, 0, ctx.st>>>((const KT*)pb.ak, pb.acoef, pb.na, slots, cap - 1);
+      k_kc_fill<KT, 2><<<gb, 256, 0, ctx.st>>>((const KT*)pb.bk, pb.bcoef, pb.nb, brec);
+    } else {  // f64 bits and int64 share the one-word layout
+      k_kc_hash_build<KT, 1><<<ga, 256, 0, ctx.st>>>((const KT*)pb.ak, pb.acoef, pb.na, slots, cap - 1);
+      k_kc_fill<KT, 1><<<gb, 256, 0, ctx.st>>>((const KT*)pb.bk, pb.bcoef, pb.nb, brec);
+    }
+    LAUNCHED(2);
     ctx.rh_key = slots;
     ctx.rh_mask = cap - 1;
+    ctx.brec = brec;
   }
   struct RowHashOff {
     Ctx& c;

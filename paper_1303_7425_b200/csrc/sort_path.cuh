@@ -75,52 +75,82 @@ k_gen_j(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __
 __device__ __forceinline__ uint32_t row_hash(uint64_t k) {
   return (uint32_t)((k * 0x9E3779B97F4A7C15ull) >> 32);
 }
-__device__ __forceinline__ uint32_t cas_row(uint32_t* p, uint32_t cmp, uint32_t v) {
-  return atomicCAS(reinterpret_cast<unsigned int*>(p), cmp, v);
-}
-__device__ __forceinline__ uint64_t cas_row(uint64_t* p, uint64_t cmp, uint64_t v) {
-  return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp,
-                   (unsigned long long)v);
-}
 
-// open-addressing table key -> row of operand a (empty slot: all-ones key);
-// key and row share one slot so a probe is a single load
-template <typename KT>
-struct alignas(2 * sizeof(KT)) RowSlot {
-  KT key;
-  uint32_t row;
+// A key and its operand coefficient in one 32-byte slot, so the segment
+// reduce gathers one sector per operand term instead of a key, a row index
+// and a coefficient from three arrays (MP n=25: 4 -> 2 sectors per pair).
+// c0/c1: f64 bits in c0; int64 in c0 (c1 its sign); int128 limbs.
+struct alignas(32) KCSlot {
+  uint64_t key;  // all-ones: empty (hash of operand a)
+  uint64_t c0, c1, pad;
 };
 
-template <typename KT>
+template <int CK>
+__device__ __forceinline__ void kc_set_coef(KCSlot& s, const void* coef, uint32_t i) {
+  if constexpr (CK == 2) {
+    s.c0 = reinterpret_cast<const uint64_t*>(coef)[2 * (uint64_t)i];
+    s.c1 = reinterpret_cast<const uint64_t*>(coef)[2 * (uint64_t)i + 1];
+  } else {
+    s.c0 = reinterpret_cast<const uint64_t*>(coef)[i];
+    s.c1 = (uint64_t)((int64_t)s.c0 >> 63);
+  }
+}
+
+// operand b as slots: brec[j] = {bk[j], bc[j]}
+template <typename KT, int CK>
 __global__ void __launch_bounds__(256)
-k_row_hash_build(const KT* __restrict__ ak, uint32_t na, RowSlot<KT>* __restrict__ slots, uint32_t mask) {
+k_kc_fill(const KT* __restrict__ bk, const void* __restrict__ bc, uint32_t nb, KCSlot* __restrict__ brec) {
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= nb) return;
+  KCSlot s;
+  s.key = (uint64_t)bk[j];
+  kc_set_coef<CK>(s, bc, j);
+  s.pad = 0;
+  brec[j] = s;
+}
+
+// open-addressing table key -> (key, coefficient) of operand a (keys of a
+// are distinct; slots pre-filled with all-ones keys)
+template <typename KT, int CK>
+__global__ void __launch_bounds__(256)
+k_kc_hash_build(const KT* __restrict__ ak, const void* __restrict__ ac, uint32_t na, KCSlot* __restrict__ slots,
+                uint32_t mask) {
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= na) return;
-  const KT key = ak[i];
-  uint32_t h = row_hash((uint64_t)key) & mask;
+  const uint64_t key = (uint64_t)ak[i];
+  uint32_t h = row_hash(key) & mask;
   for (;;) {
-    const KT prev = cas_row(&slots[h].key, (KT)~(KT)0, key);
-    if (prev == (KT)~(KT)0) {
-      slots[h].row = i;
+    const unsigned long long prev =
+        atomicCAS(reinterpret_cast<unsigned long long*>(&slots[h].key), ~0ull, (unsigned long long)key);
+    if (prev == ~0ull) {
+      kc_set_coef<CK>(slots[h], ac, i);
       return;
     }
     h = (h + 1) & mask;
   }
 }
 
-template <typename KT>
-struct RowHash {
-  const RowSlot<KT>* slots;
+struct KCHash {
+  const KCSlot* slots;
   uint32_t mask;
-  __device__ __forceinline__ uint32_t find(uint64_t key) const {
+  __device__ __forceinline__ KCSlot find(uint64_t key) const {
     uint32_t h = row_hash(key) & mask;
     for (;;) {
-      const RowSlot<KT> e = slots[h];
-      if ((uint64_t)e.key == key) return e.row;
+      const KCSlot e = slots[h];
+      if (e.key == key) return e;
       h = (h + 1) & mask;
     }
   }
 };
+
+template <int CK>
+__device__ __forceinline__ ICoef kc_icoef(const KCSlot& s) {
+  ICoef c;
+  c.x0 = s.c0;
+  c.x1 = s.c1;
+  c.x2 = (uint64_t)((int64_t)s.c1 >> 63);
+  return c;
+}
 
 // ---- K2: LSD radix sort (onesweep) ------------------------------------------
 // One upfront histogram kernel gives every pass's global digit counts (the
@@ -626,15 +656,14 @@ k_seg_reduce_f64(const KT* __restrict__ keys, const uint64_t* __restrict__ vals,
   onz[s] = (acc != 0.0) ? 1u : 0u;  // NaN != 0 -> kept, +-0 dropped (merge.py:63)
 }
 
-// K4 on j-records: the segment's key gives every pair's row through the hash
-// (a_i = key + KL - b_j), then the same folds as above.
-template <typename KT, typename RT, int NL, int CK, int G>
+// K4 on j-records: the segment's key gives every pair's a-term through the
+// key/coefficient hash (a_i = key + KL - b_j), then the same folds as above.
+template <typename RT, int NL, int CK, int G>
 __global__ void __launch_bounds__(256)
 k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ vals,
-                   const uint32_t* __restrict__ starts, uint32_t nseg, const KT* __restrict__ bk,
-                   RowHash<KT> rows, const void* __restrict__ ac, const void* __restrict__ bc, uint64_t KL,
-                   KeyPlan P, uint64_t* __restrict__ oexp, uint64_t* __restrict__ ocoef,
-                   uint32_t* __restrict__ onz) {
+                   const uint32_t* __restrict__ starts, uint32_t nseg, const KCSlot* __restrict__ brec,
+                   KCHash ahash, uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp,
+                   uint64_t* __restrict__ ocoef, uint32_t* __restrict__ onz) {
   const uint32_t s = (blockIdx.x * blockDim.x + threadIdx.x) / G;
   const uint32_t g = threadIdx.x % G;
   const bool live = s < nseg;
@@ -643,9 +672,9 @@ k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ val
   Limbs<NL> acc;
   limbs_zero(acc);
   for (uint32_t p = p0 + g; p < p1; p += G) {
-    const uint32_t j = vals[p];
-    const uint32_t i = rows.find(key - (uint64_t)__ldg(bk + j));
-    limbs_add(acc, imul<NL, CK>(load_icoef<CK>(ac, (int64_t)i), load_icoef<CK>(bc, (int64_t)j)));
+    const KCSlot b = brec[vals[p]];
+    const KCSlot a = ahash.find(key - b.key);
+    limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a), kc_icoef<CK>(b)));
   }
   if constexpr (G > 1) {
 #pragma unroll
@@ -663,12 +692,11 @@ k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ val
   onz[s] = limbs_nonzero(acc) ? 1u : 0u;
 }
 
-template <typename KT, typename RT>
+template <typename RT>
 __global__ void __launch_bounds__(256)
 k_seg_reduce_f64_j(const RT* __restrict__ keys, const uint32_t* __restrict__ vals,
-                   const uint32_t* __restrict__ starts, uint32_t nseg, const KT* __restrict__ bk,
-                   RowHash<KT> rows, const double* __restrict__ ac, const double* __restrict__ bc,
-                   uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp, double* __restrict__ ocoef,
+                   const uint32_t* __restrict__ starts, uint32_t nseg, const KCSlot* __restrict__ brec,
+                   KCHash ahash, uint64_t KL, KeyPlan P, uint64_t* __restrict__ oexp, double* __restrict__ ocoef,
                    uint32_t* __restrict__ onz) {
   uint32_t s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= nseg) return;
@@ -677,9 +705,9 @@ k_seg_reduce_f64_j(const RT* __restrict__ keys, const uint32_t* __restrict__ val
   // reference order: the stable sort kept generation order, i.e. increasing i
   double acc = 0.0;
   for (uint32_t p = p0; p < p1; ++p) {
-    const uint32_t j = vals[p];
-    const uint32_t i = rows.find(key - (uint64_t)__ldg(bk + j));
-    const double pr = __dmul_rn(__ldg(ac + i), __ldg(bc + j));
+    const KCSlot b = brec[vals[p]];
+    const KCSlot a = ahash.find(key - b.key);
+    const double pr = __dmul_rn(__longlong_as_double((long long)a.c0), __longlong_as_double((long long)b.c0));
     acc = p == p0 ? pr : __dadd_rn(acc, pr);
   }
   oexp[s] = expand_key(key, P);
