@@ -187,9 +187,22 @@ class Clocks:
 
 
 def operands(args):
+    """Synthetic operands of the config: exact ints in closed form (identical
+    to the reference's poly_from_expr output); floats as the reference builds
+    them, by repeated squaring in float (the GPU powering in its order)."""
     from paper_1303_7425_b200 import benchpolys
+    if args.coeff == "float" and _gpu_present():
+        return benchpolys.reference_float_operands(args.config)
     ct = float if args.coeff == "float" else int
     return benchpolys.CONFIGS[args.config](ct)
+
+
+def _gpu_present() -> bool:
+    try:
+        from paper_1303_7425_b200 import _native
+        return _native.load().pgpu_device_count() > 0
+    except Exception:
+        return False
 
 
 def workload_name(args, f, g):
@@ -627,7 +640,7 @@ def main():
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
                "dtype": "int64" if args.coeff == "int" else "f64",
-               "data": "synthetic (closed-form Fateman/Monagan-Pearce operands)",
+               "data": ("synthetic: closed-form Fateman/Monagan-Pearce operands (exact ints)" if args.coeff == "int" else "synthetic: the reference's float operands (repeated squaring in float, reference order)"),
                "config": {"workload": workload_name(args, f, g), "term_products": total_pairs,
                           "result_terms": n_all, "path": path_used, "result_limbs": nl,
                           "arithmetic": ("exact integers: int64 operands, 128-bit products, "

@@ -90,3 +90,22 @@ CONFIGS = {
     "mp12": lambda ct=int: monagan_pearce(12, ct),
     "mp25": lambda ct=int: monagan_pearce(25, ct),
 }
+
+
+def reference_float_operands(name: str):
+    """The reference's float operands of a config: its poly_from_expr with
+    ctype float powers the expression by repeated squaring in float
+    (io.py:215-225), so coefficients above 2^53 carry that rounding and differ
+    from the correctly rounded closed form.  Built here by the GPU powering
+    in the reference's summation order (expr.poly_from_expr), which
+    reproduces them bit for bit (tests/test_gpu_parity.py)."""
+    from .expr import poly_from_expr
+    p = int(name.lstrip("fatemanp"))
+    if name.startswith("fateman"):
+        lay = default_layout(FATEMAN_VARS)
+        base = "(1+x+y+z+t)^%d" % p
+        return poly_from_expr(base, lay, float), poly_from_expr(base + "+1", lay, float)
+    lay = default_layout(MP_VARS)
+    return (poly_from_expr("(1+x+y+2*z^2+3*t^3+5*u^5)^%d" % p, lay, float),
+            poly_from_expr("(1+u+t+2*z^2+3*y^3+5*x^5)^%d" % p, lay, float))
+

@@ -711,6 +711,9 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
       need = std::min(need, ex + 1);
     }
     pb.need_bits = need;
+    if (getenv("PGPU_DEBUG"))
+      fprintf(stderr, "[pgpu] coefficient bound: cbits %u+%u, sum|a| %.6g sum|b| %.6g max|a| %.6g max|b| %.6g -> %d bits\n",
+              hs.cbits[0], hs.cbits[1], sa, sb, ma, mb, need);
     int nl = (need + 63) / 64;
     if (nl < 1) nl = 1;
     if (nl > 3)

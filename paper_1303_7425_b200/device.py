@@ -94,6 +94,9 @@ def mul_on_device(A: DeviceOperand, B: DeviceOperand, layout, *, lo: int = 0, hi
     same operands and range (a cluster plan), or 0 to count on the device.
     inputs_on_device=False: A and B hold host pointers (pinned), copied in by
     the library (the end-to-end leg of a multi-GPU product)."""
+    if A.kind != B.kind:
+        raise ValueError(f"operands use different coefficient kinds ({A.kind} vs {B.kind}): widen the "
+                         "int64 side to int128 limbs first (Operand.from_poly(p, kind=I128))")
     lib = N.load()
     o = N.default_options()
     o.coef_kind = A.kind
