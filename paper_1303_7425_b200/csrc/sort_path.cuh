@@ -397,53 +397,57 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
 #ifndef PGPU_RS_SUPER
 #define PGPU_RS_SUPER 8
 #endif
+#ifndef PGPU_RS_MATCH
+#define PGPU_RS_MATCH 1  // 1: __match_any_sync peers; 0: eight ballots
+#endif
 constexpr int kRsSuper = PGPU_RS_SUPER;
 constexpr uint64_t kRsSuperItems = (uint64_t)kRsSuper * kRsTile;
 
 template <typename KT>
 __global__ void __launch_bounds__(kRsThreads)
 k_rs_count(const KT* __restrict__ keys, uint64_t n, int shift, uint32_t nst, uint32_t* __restrict__ cnt) {
-  __shared__ uint32_t h[kRsDigits];
+  // one histogram per warp, plain shared-memory atomics: after the first
+  // pass the digits of a warp's 32 keys rarely collide, and a warp-level
+  // match per key made the pass MIO-bound (match + atomic per key)
+  __shared__ uint32_t h[kRsWarps][kRsDigits];
   const uint32_t st = blockIdx.x;
-  h[threadIdx.x] = 0;  // kRsThreads == kRsDigits
+  const int w = threadIdx.x >> 5;
+  for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&h[0][0])[k] = 0;
   __syncthreads();
   const uint64_t b0 = (uint64_t)st * kRsSuperItems;
   const uint64_t b1 = b0 + kRsSuperItems < n ? b0 + kRsSuperItems : n;
-  const unsigned lt = lanemask_lt();
   // 16-byte loads (V keys per thread per round; b0 is a multiple of V and the
-  // arrays are 256-byte aligned), a uniform trip count for full-warp matches
+  // arrays are 256-byte aligned)
   constexpr int V = 16 / sizeof(KT);
   using Vec = typename std::conditional<sizeof(KT) == 4, uint4, ulonglong2>::type;
   const Vec* kv = reinterpret_cast<const Vec*>(keys + b0);
   const uint64_t nv = (b1 - b0 + V - 1) / V;
-#pragma unroll 2
-  for (uint64_t vb = 0; vb < nv; vb += kRsThreads) {
-    const uint64_t vi = vb + threadIdx.x;
-    KT k[V];
-    if (vi < nv && b0 + (vi + 1) * V <= b1) {
+  uint32_t* hw = h[w];
+#pragma unroll 4
+  for (uint64_t vi = threadIdx.x; vi < nv; vi += kRsThreads) {
+    if (b0 + (vi + 1) * V <= b1) {
       const Vec x = kv[vi];
       if constexpr (sizeof(KT) == 4) {
-        k[0] = x.x; k[1] = x.y; k[2] = x.z; k[3] = x.w;
+        atomicAdd(&hw[(x.x >> shift) & 0xffu], 1u);
+        atomicAdd(&hw[(x.y >> shift) & 0xffu], 1u);
+        atomicAdd(&hw[(x.z >> shift) & 0xffu], 1u);
+        atomicAdd(&hw[(x.w >> shift) & 0xffu], 1u);
       } else {
-        k[0] = x.x; k[1] = x.y;
+        atomicAdd(&hw[(unsigned)(x.x >> shift) & 0xffu], 1u);
+        atomicAdd(&hw[(unsigned)(x.y >> shift) & 0xffu], 1u);
       }
     } else {
-#pragma unroll
       for (int u = 0; u < V; ++u) {
         const uint64_t i = b0 + vi * V + u;
-        k[u] = (vi < nv && i < b1) ? keys[i] : KT(0);
+        if (i < b1) atomicAdd(&hw[(unsigned)((uint64_t)keys[i] >> shift) & 0xffu], 1u);
       }
-    }
-#pragma unroll
-    for (int u = 0; u < V; ++u) {
-      const bool ok = vi < nv && b0 + vi * V + u < b1;
-      const unsigned d = ok ? (unsigned)((uint64_t)k[u] >> shift) & 0xffu : 0x100u;
-      const unsigned peers = __match_any_sync(0xffffffffu, d);
-      if (ok && (peers & lt) == 0) atomicAdd(&h[d], (uint32_t)__popc(peers));
     }
   }
   __syncthreads();
-  cnt[(uint64_t)threadIdx.x * nst + st] = h[threadIdx.x];
+  uint32_t tot = 0;
+#pragma unroll
+  for (int q = 0; q < kRsWarps; ++q) tot += h[q][threadIdx.x];
+  cnt[(uint64_t)threadIdx.x * nst + st] = tot;
 }
 
 // CTA d: exclusive scan of cnt[d][0, nst) in place; tot[d] = the digit's total
@@ -532,7 +536,11 @@ k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restr
       const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
       const bool ok = idx < end;
       dig[k] = ok ? (unsigned)((uint64_t)key[k] >> shift) & 0xffu : 0u;
+#if PGPU_RS_MATCH
       const unsigned peers = __match_any_sync(0xffffffffu, ok ? dig[k] : 0x100u);
+#else
+      const unsigned peers = digit_peers(dig[k], __ballot_sync(0xffffffffu, ok));  // (used for valid lanes only)
+#endif
       const uint32_t c = ok ? wcnt[w][dig[k]] : 0u;
       __syncwarp();
       rank[k] = c + __popc(peers & lt);
