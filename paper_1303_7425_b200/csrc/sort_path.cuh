@@ -679,7 +679,16 @@ k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ val
   const uint64_t key = live ? (uint64_t)keys[p0] + KL : 0ull;
   Limbs<NL> acc;
   limbs_zero(acc);
-  for (uint32_t p = p0 + g; p < p1; p += G) {
+  uint32_t p = p0 + g;
+  // two pairs per iteration: both gathers of each are issued before either is used
+  for (; p + G < p1; p += 2 * G) {
+    const uint32_t j0 = vals[p], j1 = vals[p + G];
+    const KCSlot b0 = brec[j0], b1 = brec[j1];
+    const KCSlot a0 = ahash.find(key - b0.key), a1 = ahash.find(key - b1.key);
+    limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a0), kc_icoef<CK>(b0)));
+    limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a1), kc_icoef<CK>(b1)));
+  }
+  if (p < p1) {
     const KCSlot b = brec[vals[p]];
     const KCSlot a = ahash.find(key - b.key);
     limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a), kc_icoef<CK>(b)));
