@@ -478,7 +478,7 @@ __global__ void __launch_bounds__(1024) k_rs_colscan(uint32_t* __restrict__ cnt,
 }
 
 #ifndef PGPU_RS_SCAT_MINB
-#define PGPU_RS_SCAT_MINB 2
+#define PGPU_RS_SCAT_MINB 3
 #endif
 template <typename KT, typename VT = uint64_t>
 __global__ void __launch_bounds__(kRsThreads, PGPU_RS_SCAT_MINB)
@@ -503,32 +503,46 @@ k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restr
     run[d] = (unsigned long long)ex + cnt[(uint64_t)d * nst + st];
   }
   const uint64_t s0 = (uint64_t)st * kRsSuperItems;
-  // the next tile's items are loaded while this one is ranked and scattered
-  KT key[kRsIpt], nkey[kRsIpt];
-  VT val[kRsIpt], nval[kRsIpt];
-  auto load = [&](uint64_t t0, KT (&kk)[kRsIpt], VT (&vv)[kRsIpt]) {
+  // The next tile is copied into a shared-memory buffer with cp.async while
+  // this one is ranked and scattered (no registers held for it, so three
+  // CTAs fit an SM).  16-byte chunks; a partial last tile is zero-filled.
+  KT* pkey = reinterpret_cast<KT*>(rs_smem + (sizeof(KT) + sizeof(VT)) * kRsTile);  // [kRsTile]
+  VT* pval = reinterpret_cast<VT*>(rs_smem + (2 * sizeof(KT) + sizeof(VT)) * kRsTile);
+  auto prefetch = [&](uint64_t t0) {
     const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
-#pragma unroll
-    for (int k = 0; k < kRsIpt; ++k) {
-      const uint64_t idx = t0 + (uint64_t)w * (32 * kRsIpt) + k * 32 + lane;
-      const bool ok = idx < end;
-      kk[k] = ok ? kin[idx] : KT(0);
-      vv[k] = ok ? vin[idx] : VT(0);
+    constexpr int KC = 16 / sizeof(KT), VC = 16 / sizeof(VT);
+    for (int c = threadIdx.x; c < kRsTile / KC; c += kRsThreads) {
+      const uint64_t i = t0 + (uint64_t)c * KC;
+      const int bytes = i >= end ? 0 : (int)(((uint64_t)KC < end - i ? (uint64_t)KC : end - i) * sizeof(KT));
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pkey + c * KC);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(kin + (bytes ? i : 0)), "r"(bytes));
     }
+    for (int c = threadIdx.x; c < kRsTile / VC; c += kRsThreads) {
+      const uint64_t i = t0 + (uint64_t)c * VC;
+      const int bytes = i >= end ? 0 : (int)(((uint64_t)VC < end - i ? (uint64_t)VC : end - i) * sizeof(VT));
+      const uint32_t dst = (uint32_t)__cvta_generic_to_shared(pval + c * VC);
+      asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" :: "r"(dst), "l"(vin + (bytes ? i : 0)), "r"(bytes));
+    }
+    asm volatile("cp.async.commit_group;");
   };
-  if (s0 < n) load(s0, nkey, nval);
+  if (s0 < n) prefetch(s0);
+  KT key[kRsIpt];
+  VT val[kRsIpt];
   for (int tl = 0; tl < kRsSuper; ++tl) {
     const uint64_t t0 = s0 + (uint64_t)tl * kRsTile;
     if (t0 >= n) break;
     const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();  // the tile is in the buffer for every thread
 #pragma unroll
     for (int k = 0; k < kRsIpt; ++k) {
-      key[k] = nkey[k];
-      val[k] = nval[k];
+      const int q = w * (32 * kRsIpt) + k * 32 + lane;
+      key[k] = pkey[q];
+      val[k] = pval[q];
     }
-    if (tl + 1 < kRsSuper && t0 + kRsTile < n) load(t0 + kRsTile, nkey, nval);
     for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wcnt[0][0])[k] = 0;
-    __syncthreads();
+    __syncthreads();  // buffer read by all: refill it with the next tile
+    if (tl + 1 < kRsSuper && t0 + kRsTile < n) prefetch(t0 + kRsTile);
     uint32_t rank[kRsIpt];
     unsigned dig[kRsIpt];
 #pragma unroll
