@@ -112,18 +112,22 @@ def test_float_fast_mode_is_deterministic(name, path):
         assert np.array_equal(r.coef_array().view(np.uint64), c0)
 
 
+@pytest.mark.parametrize("path", ["auto", "bucket", "sort"])
 @pytest.mark.parametrize("ordered", [None, False])
-def test_mp12_float_auto_equals_reference_digest(ordered):
-    """Sparse products fold each term in increasing row (the bucket path's
-    owner fold): the default mode, and the fast mode too, give the
-    reference's result bit for bit on the bucket path."""
+def test_mp12_float_sparse_paths_equal_reference_digest(path, ordered):
+    """Sparse products fold each term in increasing row on the bucket path
+    (owner fold in (key, row) order) and on the sort path (stable radix
+    order): the default mode, and the fast mode too, give the reference's
+    result bit for bit."""
     from paper_1303_7425_b200.parmul import Operand, native_mul
     f, g = benchpolys.CONFIGS["mp12"](float)
-    p = mul(f, g, MulConfig(float_ordered=ordered))
+    p = mul(f, g, MulConfig(path=path, float_ordered=ordered))
     want = digests()["products"]["mp12/float"]
     assert p.n == want["n"] and io.poly_digest(p) == want["sha256"]
-    raw = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, float_ordered=bool(ordered))
-    assert raw.path == "bucket"
+    if path != "auto":
+        raw = native_mul(Operand.from_poly(f), Operand.from_poly(g), f.layout, path=path,
+                         float_ordered=bool(ordered))
+        assert raw.path == path
 
 
 def test_default_float_mode_is_the_reference_order():
