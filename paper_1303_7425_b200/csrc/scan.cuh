@@ -77,6 +77,21 @@ k_range_scan(uint64_t n, uint64_t per, Gen gen, Out out, const T* part) {
   }
 }
 
+// Sum of gen(i) over [0, n) (the first two kernels of device_scan); the total
+// lands in part[*g_out].  Returns the number of kernel launches (2).
+template <typename T, typename Gen>
+int device_sum(uint64_t n, Gen gen, T* part, int* g_out, cudaStream_t st) {
+  uint64_t per = (uint64_t)kScanTile * 4;
+  if ((n + per - 1) / per > (uint64_t)kMaxScanBlocks) per = (n + kMaxScanBlocks - 1) / kMaxScanBlocks;
+  per = (per + kScanTile - 1) / kScanTile * kScanTile;
+  int g = (int)((n + per - 1) / per);
+  if (g < 1) g = 1;
+  k_range_reduce<T><<<g, kScanThreads, 0, st>>>(n, per, gen, part);
+  k_part_scan<T><<<1, 1024, 0, st>>>(part, g);
+  *g_out = g;
+  return 2;
+}
+
 // Host driver.  `part` must hold >= kMaxScanBlocks+1 elements.
 // Returns the number of kernel launches (3).  The total lands in part[*g_out].
 template <typename T, typename Gen, typename Out>
