@@ -26,10 +26,11 @@ full() {  # kernel-regex config coeff skip: capture, summarise here, keep the re
 if [ -z "$NO_FULL" ]; then
   KEEP_REP=1 full k_numeric fateman30 int 1
   full k_symbolic fateman30 int 1
-  full k_bucket_reduce mp12 int 1
-  full k_bin_scatter mp12 int 1
-  full k_bin_count mp12 int 2
-  full k_rs_onesweep mp25 int 40
+  full k_rs_scatter mp12 int 4
+  full k_rs_count mp12 int 4
+  full k_seg_reduce_int_j mp12 int 1
+  full k_rs_scatter mp25 int 40
+  full k_rs_count mp25 int 40
   full k_gen_j mp25 int 12
   full k_seg_reduce_int_j mp25 int 12
 fi
