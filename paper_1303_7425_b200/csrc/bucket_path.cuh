@@ -201,9 +201,6 @@ constexpr int kBkIpt = kBucketCap / kBucketThreads;  // records per thread
 constexpr int kBkTable = 2 * kBucketCap;             // hash slots (load factor <= 1/2)
 constexpr int kBkSlotBits = 12;
 static_assert(kBkTable <= (1 << kBkSlotBits), "slot index must fit the sort word");
-constexpr unsigned long long kBkAgg = 1ull << 62;    // look-back flags (value in the low 62 bits)
-constexpr unsigned long long kBkPre = 2ull << 62;
-constexpr unsigned long long kBkVal = (1ull << 62) - 1;
 constexpr uint32_t kBkRankThreads = kBucketThreads - 32;  // warp 0 runs the look-back meanwhile
 
 struct BucketArgs {
@@ -397,45 +394,6 @@ __device__ __forceinline__ void rank_counting(BucketSmem<KT, NL, ROWS>& S, uint3
   }
 }
 
-// decoupled look-back (warp 0): publish this bucket's distinct-key count,
-// return the exclusive prefix of the counts of the buckets before it.  The
-// warp reads 32 predecessors per round trip: it consumes the aggregates up to
-// the nearest inclusive prefix, or up to the first predecessor not yet
-// published (re-polled from there).
-__device__ __forceinline__ unsigned long long bucket_lookback(unsigned long long* status, uint32_t k,
-                                                              uint32_t agg) {
-  const int lane = threadIdx.x & 31;
-  volatile unsigned long long* st = status + k;
-  if (k == 0) {
-    if (lane == 0) *st = kBkPre | agg;
-    return 0;
-  }
-  if (lane == 0) *st = kBkAgg | agg;
-  unsigned long long excl = 0;
-  int64_t q = (int64_t)k - 1;  // nearest predecessor not yet consumed
-  for (;;) {
-    const int64_t idx = q - lane;
-    const unsigned long long v =
-        idx >= 0 ? *(volatile unsigned long long*)(status + idx) : (unsigned long long)kBkPre;
-    const unsigned long long flag = v & ~kBkVal;
-    const unsigned pre = __ballot_sync(0xffffffffu, flag == kBkPre);
-    const unsigned notready = __ballot_sync(0xffffffffu, flag == 0);
-    const int first_pre = pre ? __ffs(pre) - 1 : 32;
-    const unsigned upto = first_pre == 32 ? 0xffffffffu : ((2u << first_pre) - 1u);
-    const unsigned wait = notready & upto;
-    // lanes [0, take) are consumed: published aggregates, plus the prefix if no gap
-    const int take = wait ? __ffs(wait) - 1 : (first_pre == 32 ? 32 : first_pre + 1);
-    unsigned long long part = lane < take ? (v & kBkVal) : 0ull;
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
-    excl += part;
-    q -= take;
-    if (!wait && first_pre < 32) break;
-  }
-  if (lane == 0) *st = kBkPre | (excl + agg);
-  return excl;
-}
-
 // CK: 0 f64, 1 int64, 2 int128 operands; NL result limbs
 #ifndef PGPU_BUCKET_MINB
 #define PGPU_BUCKET_MINB (768 / PGPU_BUCKET_THREADS)
@@ -464,7 +422,7 @@ k_bucket_reduce(BucketArgs A) {
       if (threadIdx.x == 0) {
         *A.overflow = 1u;
         volatile unsigned long long* st = A.status + k;
-        *st = (k == 0 ? kBkPre : kBkAgg) | 0ull;
+        *st = (k == 0 ? kLbPre : kLbAgg) | 0ull;
       }
       continue;
     }
@@ -525,7 +483,7 @@ k_bucket_reduce(BucketArgs A) {
     // 3. output base (warp 0, look-back) while the other warps rank the keys
     if (nd <= 2u * kBkRankThreads) {
       if (threadIdx.x < 32) {
-        const unsigned long long b = bucket_lookback(A.status, k, nd);
+        const unsigned long long b = tile_lookback(A.status, k, nd);
         if (threadIdx.x == 0) S.base = b;
       } else if (nd <= kBkRankThreads) {
         rank_counting<KT, NL, ROWS, 1>(S, nd);
@@ -551,7 +509,7 @@ k_bucket_reduce(BucketArgs A) {
         if (threadIdx.x + c * kBucketThreads < nd) S.keyr[rk[c]] = kk[c];
     } else {
       if (threadIdx.x < 32) {
-        const unsigned long long b = bucket_lookback(A.status, k, nd);
+        const unsigned long long b = tile_lookback(A.status, k, nd);
         if (threadIdx.x == 0) S.base = b;
       }
       if (nd <= 4u * kBucketThreads) rank_sorted<KT, NL, ROWS, 4>(S, nd);

@@ -92,6 +92,50 @@ int device_sum(uint64_t n, Gen gen, T* part, int* g_out, cudaStream_t st) {
   return 2;
 }
 
+constexpr unsigned long long kLbAgg = 1ull << 62;
+constexpr unsigned long long kLbPre = 2ull << 62;
+constexpr unsigned long long kLbVal = (1ull << 62) - 1;
+
+// Decoupled look-back (called by one whole warp): publish tile k's count and
+// return the exclusive prefix of the counts of tiles 0..k-1 (tiles claimed in
+// order).  The warp reads 32 predecessors per round trip: it consumes the
+// aggregates up to the nearest inclusive prefix, or up to the first
+// predecessor not yet published (re-polled from there).  status[] is zeroed
+// before the launch; a word holds a flag (kLbAgg / kLbPre) and a 62-bit value.
+__device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* status, uint32_t k,
+                                                              uint32_t agg) {
+  const int lane = threadIdx.x & 31;
+  volatile unsigned long long* st = status + k;
+  if (k == 0) {
+    if (lane == 0) *st = kLbPre | agg;
+    return 0;
+  }
+  if (lane == 0) *st = kLbAgg | agg;
+  unsigned long long excl = 0;
+  int64_t q = (int64_t)k - 1;  // nearest predecessor not yet consumed
+  for (;;) {
+    const int64_t idx = q - lane;
+    const unsigned long long v =
+        idx >= 0 ? *(volatile unsigned long long*)(status + idx) : (unsigned long long)kLbPre;
+    const unsigned long long flag = v & ~kLbVal;
+    const unsigned pre = __ballot_sync(0xffffffffu, flag == kLbPre);
+    const unsigned notready = __ballot_sync(0xffffffffu, flag == 0);
+    const int first_pre = pre ? __ffs(pre) - 1 : 32;
+    const unsigned upto = first_pre == 32 ? 0xffffffffu : ((2u << first_pre) - 1u);
+    const unsigned wait = notready & upto;
+    // lanes [0, take) are consumed: published aggregates, plus the prefix if no gap
+    const int take = wait ? __ffs(wait) - 1 : (first_pre == 32 ? 32 : first_pre + 1);
+    unsigned long long part = lane < take ? (v & kLbVal) : 0ull;
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) part += __shfl_xor_sync(0xffffffffu, part, d);
+    excl += part;
+    q -= take;
+    if (!wait && first_pre < 32) break;
+  }
+  if (lane == 0) *st = kLbPre | (excl + agg);
+  return excl;
+}
+
 // Host driver.  `part` must hold >= kMaxScanBlocks+1 elements.
 // Returns the number of kernel launches (3).  The total lands in part[*g_out].
 template <typename T, typename Gen, typename Out>
