@@ -17,15 +17,18 @@
 //   B3 k_bin_scatter  the same walk writes (key - KL, i<<32|j) once, at
 //                     offset(bin) + atomic run position: records of one bucket
 //                     are contiguous
-//   B4 k_bucket_reduce persistent CTAs claim buckets in key order: keys
-//                     grouped in a shared-memory table (CAS on keys only),
-//                     distinct keys ranked, records placed in (key, row)
+//   B4 k_bucket_reduce persistent CTAs claim buckets in key order: each
+//                     distinct key ranked (a bitmap over the bucket's key
+//                     span with a popcount prefix per word; a shared-memory
+//                     hash for buckets spanning more than kBkWords*32 keys),
+//                     records placed in (key, row)
 //                     order, products folded by one owner per key in that
 //                     order (no atomics on coefficient data: integers exact,
 //                     doubles in the reference's order and run-to-run
-//                     identical), zero sums dropped (merge.py:63); a decoupled
-//                     look-back over the buckets' term counts places the terms
-//                     at their final positions.  A bin above the bucket bound
+//                     identical), zero sums dropped (merge.py:63); terms go
+//                     to their final positions: the CTA's previous bucket's
+//                     inclusive prefix plus the published term counts of the
+//                     buckets claimed in between.  A bin above the bucket bound
 //                     sends the batch to the sort path.
 //
 // DRAM traffic per pair: one record write + one record read (12-16 B each),
@@ -181,22 +184,29 @@ struct BStartOut {
 // ---- B4 ---------------------------------------------------------------------
 // Persistent CTAs claim buckets in key order.  A bucket's records are grouped
 // by key without touching coefficient data atomically:
-//   1. keys -> open-addressing slots (CAS on the key only; equal keys share a slot)
-//   2. distinct keys compacted; their count is published at once for a
-//      decoupled look-back over the buckets (warp 0 resolves the bucket's
-//      output base while the other warps rank the keys)
-//   3. the distinct keys are ranked (counting rank, or a bitonic sort above 224)
+//   1-3. every record gets its key's rank among the bucket's distinct keys.
+//      Bitmap (keys spanning <= kBkWords*32 values, the common case): one
+//      shared-memory atomicOr per record sets bit key - lo, a block scan of
+//      the words' popcounts gives each word's rank base, and a record's rank
+//      is base + popc(word & bits below its key): no comparisons.  Hash
+//      (wider spans): keys -> open-addressing slots (CAS on the key only),
+//      distinct keys compacted and ranked (counting rank, or a bitonic sort
+//      above 224).  The distinct-key count is published at once (successors
+//      need it for their output base)
 //   4. per key rank: record count (the returned index is an arbitrary position
 //      in the key's run), exclusive scan -> run starts; each record's position
 //      in (key, row) order: floats rank their row among the run's rows (the
 //      reference's tie order, merge.py:32-33), integers keep the arbitrary
 //      position (exact sums do not depend on the order)
-//   5. each record's product is written at its position; one owner per key
-//      folds its run in order (acc = p_first; acc += p ...; merge.py:49-58)
-//   6. term r of the bucket goes to base + r (bucket order = key order): no
-//      staging and no gather pass.  A zero sum (merge.py:63) leaves its slot
-//      marked with the all-ones exponent (SENTINEL, never a term) and is
-//      counted; the driver compacts only if any occurred.
+//   5. each record's product is written at its position; warp 0 then resolves
+//      the bucket's output base (bucket_base: this CTA's previous inclusive
+//      prefix + the counts of the buckets claimed in between, one round of
+//      loads instead of a look-back walk over buckets in flight)
+//   6. one owner per key folds its run in order (acc = p_first; acc += p ...;
+//      merge.py:49-58) and writes term base + rank: no staging and no gather
+//      pass.  A zero sum (merge.py:63) leaves its slot marked with the
+//      all-ones exponent (SENTINEL, never a term) and is counted; the driver
+//      compacts only if any occurred.
 constexpr int kBkIpt = kBucketCap / kBucketThreads;  // records per thread
 constexpr int kBkTable = 2 * kBucketCap;             // hash slots (load factor <= 1/2)
 constexpr int kBkSlotBits = 12;
@@ -221,10 +231,26 @@ struct BucketArgs {
   unsigned long long* zeros;   // zero sums written as holes
 };
 
+// Buckets whose keys span at most kBkWords*32 values rank them with a bitmap
+// (one bit per key of the span, popcount prefix per word); wider ones hash.
+#ifndef PGPU_BK_WORDS
+#define PGPU_BK_WORDS (PGPU_BUCKET_CAP >= 2048 ? 2048 : 1024)
+#endif
+constexpr int kBkWords = PGPU_BK_WORDS;
+static_assert(kBkWords % kBucketThreads == 0, "whole words per thread");
+
 template <typename KT, int NL, bool ROWS>
 struct BucketSmem {
-  KT hkey[kBkTable];                 // open-addressing key table
-  uint16_t rank[kBkTable];           // key rank of an occupied slot
+  union {
+    struct {
+      KT hkey[kBkTable];             // open-addressing key table
+      uint16_t rank[kBkTable];       // key rank of an occupied slot
+    } h;
+    struct {
+      uint32_t bits[kBkWords];       // key k - lo present: bit (k - lo) & 31 of word (k - lo) >> 5
+      uint16_t wpre[kBkWords];       // distinct keys before the word
+    } m;
+  };
   union {
     uint64_t sortv[kBucketCap];      // distinct keys: key << 12 | slot
     uint64_t prod[kBucketCap * NL];  // products at their (key, row) positions; then run sums
@@ -233,6 +259,7 @@ struct BucketSmem {
   uint32_t start[kBucketCap + 1];    // per key rank: count, then run start
   uint32_t rows[ROWS ? kBucketCap : 1];  // rows at arbitrary run positions (f64 tie order)
   uint32_t sh[33];
+  KT kext[2][kBucketThreads / 32];   // per-warp key minimum / maximum
   uint32_t bucket;
   unsigned long long base;
 };
@@ -243,6 +270,65 @@ __device__ __forceinline__ uint32_t cas_key(uint32_t* p, uint32_t cmp, uint32_t 
 __device__ __forceinline__ uint64_t cas_key(uint64_t* p, uint64_t cmp, uint64_t v) {
   return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)cmp,
                    (unsigned long long)v);
+}
+
+// Bucket status words (zeroed before the launch): bit 63 = the bucket's term
+// count is published (bits 0-15); bit 62 = its inclusive prefix too (bits
+// 16-61, read by the host for the last bucket).
+constexpr unsigned long long kBsCnt = 1ull << 63;
+constexpr unsigned long long kBsIncl = 1ull << 62;
+
+__device__ __forceinline__ void bucket_publish(unsigned long long* status, uint32_t k, uint32_t nd) {
+  *(volatile unsigned long long*)(status + k) = kBsCnt | nd;
+}
+
+// Output base of bucket k (one whole warp).  Every CTA knows the inclusive
+// prefix of its own previous bucket kp (kp = -1: prefix 0), so the base is
+// that prefix plus the counts of the buckets claimed in between -- published
+// as soon as each bucket has ranked its keys.  The warp loads them all at once
+// (16 per lane per round, ~one bucket per resident CTA in between): one L2
+// round trip instead of a look-back walk over buckets still in flight.
+__device__ __forceinline__ unsigned long long bucket_base(const unsigned long long* status, uint32_t k,
+                                                          int64_t kp, unsigned long long pre) {
+  constexpr int U = 16;
+  const int lane = threadIdx.x & 31;
+  unsigned long long sum = 0;
+  for (int64_t j0 = kp + 1; j0 < (int64_t)k; j0 += 32 * U) {
+    unsigned long long v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + lane + 32 * u;
+      v[u] = j < (int64_t)k ? *(const volatile unsigned long long*)(status + j) : kBsCnt;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t j = j0 + lane + 32 * u;
+      while (!(v[u] & kBsCnt)) v[u] = *(const volatile unsigned long long*)(status + j);
+      sum += v[u] & 0xffffull;
+    }
+  }
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, d);
+  return pre + sum;
+}
+
+__device__ __forceinline__ uint32_t warp_min_key(uint32_t v) { return __reduce_min_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint32_t warp_max_key(uint32_t v) { return __reduce_max_sync(0xffffffffu, v); }
+__device__ __forceinline__ uint64_t warp_min_key(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o < v ? o : v;
+  }
+  return v;
+}
+__device__ __forceinline__ uint64_t warp_max_key(uint64_t v) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    const uint64_t o = __shfl_xor_sync(0xffffffffu, v, d);
+    v = o > v ? o : v;
+  }
+  return v;
 }
 
 __device__ __forceinline__ uint32_t bucket_hash(uint64_t k) {
@@ -345,7 +431,7 @@ __device__ __forceinline__ void rank_sorted(BucketSmem<KT, NL, ROWS>& S, uint32_
   for (int e = 0; e < E; ++e) {
     const uint32_t x = threadIdx.x * E + e;
     if (x < nd) {
-      S.rank[v[e] & ((1u << kBkSlotBits) - 1)] = (uint16_t)x;
+      S.h.rank[v[e] & ((1u << kBkSlotBits) - 1)] = (uint16_t)x;
       S.keyr[x] = (KT)(v[e] >> kBkSlotBits);
     }
   }
@@ -390,7 +476,7 @@ __device__ __forceinline__ void rank_counting(BucketSmem<KT, NL, ROWS>& S, uint3
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const uint32_t x = t + c * kBkRankThreads;
-    if (x < nd) S.rank[S.sortv[x] & ((1u << kBkSlotBits) - 1)] = (uint16_t)rk[c];
+    if (x < nd) S.h.rank[S.sortv[x] & ((1u << kBkSlotBits) - 1)] = (uint16_t)rk[c];
   }
 }
 
@@ -405,11 +491,16 @@ k_bucket_reduce(BucketArgs A) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
   BucketSmem<KT, NL, ROWS>& S = *reinterpret_cast<BucketSmem<KT, NL, ROWS>*>(smem_raw);
   const KT kEmpty = (KT)~(KT)0;
+  int64_t kp = -1;             // this CTA's previous bucket
+  unsigned long long pre = 0;  // and its inclusive term prefix
   for (;;) {
     __syncthreads();  // the previous bucket's readers are done with the shared state
     if (threadIdx.x == 0) S.bucket = atomicAdd(A.ticket, 1u);
+    // the key bitmap starts clear (the common case; the hash table is set up
+    // only by the buckets that need it)
 #pragma unroll
-    for (int u = 0; u < kBkTable / kBucketThreads; ++u) S.hkey[threadIdx.x + u * kBucketThreads] = kEmpty;
+    for (int u = 0; u < kBkWords / (4 * kBucketThreads); ++u)
+      reinterpret_cast<uint4*>(S.m.bits)[threadIdx.x + u * kBucketThreads] = make_uint4(0, 0, 0, 0);
     for (uint32_t x = threadIdx.x; x <= (uint32_t)kBucketCap; x += kBucketThreads) S.start[x] = 0;
     __syncthreads();
     const uint32_t k = S.bucket;
@@ -421,110 +512,183 @@ k_bucket_reduce(BucketArgs A) {
     if (n > (uint32_t)kBucketCap) {  // one fine bin above the bucket bound
       if (threadIdx.x == 0) {
         *A.overflow = 1u;
-        volatile unsigned long long* st = A.status + k;
-        *st = (k == 0 ? kLbPre : kLbAgg) | 0ull;
+        bucket_publish(A.status, k, 0);
       }
       continue;
     }
-    // records (coalesced), 1. slot per distinct key
+    // records (coalesced) and the bucket's key extent
     uint64_t id[kBkIpt];
-    uint32_t slot[kBkIpt];
+    uint32_t slot[kBkIpt];  // the record's key rank after step 3
     uint32_t valid = 0;
+    KT key[kBkIpt];
     {
       const KT* __restrict__ rkey = reinterpret_cast<const KT*>(A.rkey) + r0;
       const uint64_t* __restrict__ rid = A.rid + r0;
-      KT key[kBkIpt];
+      KT lmin = kEmpty, lmax = 0;
 #pragma unroll
       for (int u = 0; u < kBkIpt; ++u) {
         const uint32_t q = threadIdx.x + u * kBucketThreads;
         key[u] = q < n ? rkey[q] : kEmpty;
         id[u] = q < n ? rid[q] : 0ull;
         valid |= (q < n ? 1u : 0u) << u;
+        if (q < n) {
+          lmin = key[u] < lmin ? key[u] : lmin;
+          lmax = key[u] > lmax ? key[u] : lmax;
+        }
       }
+      lmin = warp_min_key(lmin);
+      lmax = warp_max_key(lmax);
+      if ((threadIdx.x & 31) == 0) {
+        S.kext[0][threadIdx.x >> 5] = lmin;
+        S.kext[1][threadIdx.x >> 5] = lmax;
+      }
+    }
+    __syncthreads();
+    KT kmin = S.kext[0][0], kmax = S.kext[1][0];
+#pragma unroll
+    for (int q = 1; q < kBucketThreads / 32; ++q) {
+      kmin = S.kext[0][q] < kmin ? S.kext[0][q] : kmin;
+      kmax = S.kext[1][q] > kmax ? S.kext[1][q] : kmax;
+    }
+    const KT lo = kmin & ~(KT)31;
+    uint32_t nd;
+    if (n == 0 || (uint64_t)(kmax - lo) < 32ull * kBkWords) {
+      // 1-3 (bitmap): mark each key's bit; a key's rank is the number of marked
+      // bits before it (popcount prefix per word); no comparisons
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u)
+        if ((valid >> u) & 1u) {
+          const uint32_t off = (uint32_t)(key[u] - lo);
+          atomicOr(&S.m.bits[off >> 5], 1u << (off & 31));
+        }
+      __syncthreads();
+      constexpr int WPT = kBkWords / kBucketThreads;  // consecutive words per thread
+      static_assert(WPT % 8 == 0 || WPT == 4, "whole 16-byte loads and stores per thread");
+      uint32_t c[WPT];
+      {
+        const uint4* bw = reinterpret_cast<const uint4*>(S.m.bits) + (WPT / 4) * threadIdx.x;
+#pragma unroll
+        for (int q = 0; q < WPT / 4; ++q) {
+          const uint4 x = bw[q];
+          c[4 * q] = __popc(x.x);
+          c[4 * q + 1] = __popc(x.y);
+          c[4 * q + 2] = __popc(x.z);
+          c[4 * q + 3] = __popc(x.w);
+        }
+      }
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int q = 0; q < WPT; ++q) cnt += c[q];
+      uint32_t ex = block_excl_scan(cnt, S.sh, &nd);
+      uint32_t pw[WPT / 2];
+#pragma unroll
+      for (int q = 0; q < WPT; q += 2) {
+        pw[q / 2] = ex | ((ex + c[q]) << 16);
+        ex += c[q] + c[q + 1];
+      }
+      if constexpr (WPT == 4) {
+        reinterpret_cast<uint2*>(S.m.wpre)[threadIdx.x] = make_uint2(pw[0], pw[1]);
+      } else {
+#pragma unroll
+        for (int q = 0; q < WPT / 8; ++q)
+          reinterpret_cast<uint4*>(S.m.wpre)[(WPT / 8) * threadIdx.x + q] =
+              make_uint4(pw[4 * q], pw[4 * q + 1], pw[4 * q + 2], pw[4 * q + 3]);
+      }
+      __syncthreads();
+      // the bucket's term count goes out now (its successors' bases need it)
+      if (threadIdx.x == 0) bucket_publish(A.status, k, nd);
+#pragma unroll
+      for (int u = 0; u < kBkIpt; ++u)
+        if ((valid >> u) & 1u) {
+          const uint32_t off = (uint32_t)(key[u] - lo);
+          const uint32_t wd = off >> 5;
+          slot[u] = S.m.wpre[wd] + __popc(S.m.bits[wd] & ((1u << (off & 31)) - 1u));
+          S.keyr[slot[u]] = key[u];  // (every record of the key writes the same value)
+        }
+    } else {
+      // 1. slot per distinct key (open addressing, CAS on the key only)
+#pragma unroll
+      for (int u = 0; u < kBkTable / kBucketThreads; ++u) S.h.hkey[threadIdx.x + u * kBucketThreads] = kEmpty;
+      __syncthreads();
 #pragma unroll
       for (int u = 0; u < kBkIpt; ++u) {
         uint32_t h = 0;
         if ((valid >> u) & 1u) {
           h = bucket_hash((uint64_t)key[u]);
           for (;;) {
-            const KT prev = cas_key(&S.hkey[h], kEmpty, key[u]);
+            const KT prev = cas_key(&S.h.hkey[h], kEmpty, key[u]);
             if (prev == kEmpty || prev == key[u]) break;
             h = (h + 1) & (kBkTable - 1);
           }
         }
         slot[u] = h;
       }
-    }
-    __syncthreads();
-    // 2. distinct keys compacted in slot order (thread t scans slots [16t, 16t+16))
-    constexpr int TPT = kBkTable / kBucketThreads;
-    uint32_t nd;
-    {
-      const uint32_t t0 = threadIdx.x * TPT;
-      uint32_t occ = 0, cnt = 0;
+      __syncthreads();
+      // 2. distinct keys compacted in slot order (thread t scans slots [16t, 16t+16))
+      constexpr int TPT = kBkTable / kBucketThreads;
+      {
+        const uint32_t t0 = threadIdx.x * TPT;
+        uint32_t occ = 0, cnt = 0;
 #pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        const bool o = S.hkey[t0 + u] != kEmpty;
-        occ |= (o ? 1u : 0u) << u;
-        cnt += o ? 1u : 0u;
-      }
-      uint32_t at = block_excl_scan(cnt, S.sh, &nd);
+        for (int u = 0; u < TPT; ++u) {
+          const bool o = S.h.hkey[t0 + u] != kEmpty;
+          occ |= (o ? 1u : 0u) << u;
+          cnt += o ? 1u : 0u;
+        }
+        uint32_t at = block_excl_scan(cnt, S.sh, &nd);
 #pragma unroll
-      for (int u = 0; u < TPT; ++u) {
-        if ((occ >> u) & 1u) {
-          const KT kk = S.hkey[t0 + u];
-          S.sortv[at] = ((uint64_t)kk << kBkSlotBits) | (t0 + u);
-          S.keyr[at] = kk;  // slot order (counting rank input); rank order after step 3
-          ++at;
+        for (int u = 0; u < TPT; ++u) {
+          if ((occ >> u) & 1u) {
+            const KT kk = S.h.hkey[t0 + u];
+            S.sortv[at] = ((uint64_t)kk << kBkSlotBits) | (t0 + u);
+            S.keyr[at] = kk;  // slot order (counting rank input); rank order after step 3
+            ++at;
+          }
         }
       }
-    }
-    __syncthreads();
-    // 3. output base (warp 0, look-back) while the other warps rank the keys
-    if (nd <= 2u * kBkRankThreads) {
-      if (threadIdx.x < 32) {
-        const unsigned long long b = tile_lookback(A.status, k, nd);
-        if (threadIdx.x == 0) S.base = b;
-      } else if (nd <= kBkRankThreads) {
-        rank_counting<KT, NL, ROWS, 1>(S, nd);
+      __syncthreads();
+      // 3. the term count goes out (warp 0) while the other warps rank the keys
+      if (nd <= 2u * kBkRankThreads) {
+        if (threadIdx.x < 32) {
+          if (threadIdx.x == 0) bucket_publish(A.status, k, nd);
+        } else if (nd <= kBkRankThreads) {
+          rank_counting<KT, NL, ROWS, 1>(S, nd);
+        } else {
+          rank_counting<KT, NL, ROWS, 2>(S, nd);
+        }
+        __syncthreads();
+        // keys in rank order (keyr held them in slot order for the counting rank)
+        constexpr int RC = (2 * kBkRankThreads + kBucketThreads - 1) / kBucketThreads;
+        KT kk[RC];
+        uint32_t rk[RC];
+#pragma unroll
+        for (int c = 0; c < RC; ++c) {
+          const uint32_t x = threadIdx.x + c * kBucketThreads;
+          if (x < nd) {
+            kk[c] = S.keyr[x];
+            rk[c] = S.h.rank[S.sortv[x] & ((1u << kBkSlotBits) - 1)];
+          }
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < RC; ++c)
+          if (threadIdx.x + c * kBucketThreads < nd) S.keyr[rk[c]] = kk[c];
       } else {
-        rank_counting<KT, NL, ROWS, 2>(S, nd);
-      }
-      __syncthreads();
-      // keys in rank order (keyr held them in slot order for the counting rank)
-      constexpr int RC = (2 * kBkRankThreads + kBucketThreads - 1) / kBucketThreads;
-      KT kk[RC];
-      uint32_t rk[RC];
-#pragma unroll
-      for (int c = 0; c < RC; ++c) {
-        const uint32_t x = threadIdx.x + c * kBucketThreads;
-        if (x < nd) {
-          kk[c] = S.keyr[x];
-          rk[c] = S.rank[S.sortv[x] & ((1u << kBkSlotBits) - 1)];
-        }
+        if (threadIdx.x == 0) bucket_publish(A.status, k, nd);
+        if (nd <= 4u * kBucketThreads) rank_sorted<KT, NL, ROWS, 4>(S, nd);
+        else rank_sorted<KT, NL, ROWS, 8>(S, nd);
       }
       __syncthreads();
 #pragma unroll
-      for (int c = 0; c < RC; ++c)
-        if (threadIdx.x + c * kBucketThreads < nd) S.keyr[rk[c]] = kk[c];
-    } else {
-      if (threadIdx.x < 32) {
-        const unsigned long long b = tile_lookback(A.status, k, nd);
-        if (threadIdx.x == 0) S.base = b;
-      }
-      if (nd <= 4u * kBucketThreads) rank_sorted<KT, NL, ROWS, 4>(S, nd);
-      else rank_sorted<KT, NL, ROWS, 8>(S, nd);
+      for (int u = 0; u < kBkIpt; ++u)
+        if ((valid >> u) & 1u) slot[u] = S.h.rank[slot[u]];  // slot -> key rank
     }
     __syncthreads();
     // 4. runs: count per key rank (the index is an arbitrary position in the run)
     uint32_t pos[kBkIpt];
 #pragma unroll
-    for (int u = 0; u < kBkIpt; ++u) {
-      if ((valid >> u) & 1u) {
-        slot[u] = S.rank[slot[u]];  // slot -> key rank
-        pos[u] = atomicAdd(&S.start[slot[u]], 1u);
-      }
-    }
+    for (int u = 0; u < kBkIpt; ++u)
+      if ((valid >> u) & 1u) pos[u] = atomicAdd(&S.start[slot[u]], 1u);
     if (threadIdx.x == 0) S.start[nd] = n;
     __syncthreads();
     chunk_scan<kBkIpt>(S.start, nd, S.sh);
@@ -568,9 +732,19 @@ k_bucket_reduce(BucketArgs A) {
         for (int w = 0; w < NL; ++w) S.prod[(size_t)pos[u] * NL + w] = pr.w[w];
       }
     }
+    // output base (warp 0, after its products; the barrier below waits for it)
+    if (threadIdx.x < 32) {
+      const unsigned long long b = bucket_base(A.status, k, kp, pre);
+      if (threadIdx.x == 0) {
+        S.base = b;
+        *(volatile unsigned long long*)(A.status + k) = kBsCnt | kBsIncl | ((b + nd) << 16) | nd;
+      }
+    }
     __syncthreads();
     // 6. one owner per key folds its run in order and writes term base + rank
     const unsigned long long base = S.base;
+    kp = k;
+    pre = base + nd;
     uint32_t nzero = 0;
     for (uint32_t r = threadIdx.x; r < nd; r += kBucketThreads) {
       const uint32_t s0 = S.start[r], s1 = S.start[r + 1];

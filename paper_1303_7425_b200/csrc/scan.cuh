@@ -96,21 +96,25 @@ constexpr unsigned long long kLbAgg = 1ull << 62;
 constexpr unsigned long long kLbPre = 2ull << 62;
 constexpr unsigned long long kLbVal = (1ull << 62) - 1;
 
-// Decoupled look-back (called by one whole warp): publish tile k's count and
-// return the exclusive prefix of the counts of tiles 0..k-1 (tiles claimed in
-// order).  The warp reads 32 predecessors per round trip: it consumes the
-// aggregates up to the nearest inclusive prefix, or up to the first
-// predecessor not yet published (re-polled from there).  status[] is zeroed
-// before the launch; a word holds a flag (kLbAgg / kLbPre) and a 62-bit value.
-__device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* status, uint32_t k,
-                                                              uint32_t agg) {
+// Decoupled look-back.  status[] is zeroed before the launch; a word holds a
+// flag (kLbAgg / kLbPre) and a 62-bit value.  Tiles are claimed in order.
+//
+// tile_publish (one thread): tile k's count, as soon as it is known (tile 0:
+// its inclusive prefix at once).
+__device__ __forceinline__ void tile_publish(unsigned long long* status, uint32_t k, uint32_t agg) {
+  *(volatile unsigned long long*)(status + k) = (k == 0 ? kLbPre : kLbAgg) | agg;
+}
+
+// tile_resolve (one whole warp): the exclusive prefix of the counts of tiles
+// 0..k-1; with `finish`, lane 0 then publishes tile k's inclusive prefix.
+// The warp reads 32 predecessors per round trip: it consumes the aggregates
+// up to the nearest inclusive prefix, or up to the first predecessor not yet
+// published (re-polled from there).  (Eight groups of 32 loads per round
+// made the MP n=12 head scan 1.7x slower.)
+__device__ __forceinline__ unsigned long long tile_resolve(unsigned long long* status, uint32_t k,
+                                                           uint32_t agg, bool finish) {
   const int lane = threadIdx.x & 31;
-  volatile unsigned long long* st = status + k;
-  if (k == 0) {
-    if (lane == 0) *st = kLbPre | agg;
-    return 0;
-  }
-  if (lane == 0) *st = kLbAgg | agg;
+  if (k == 0) return 0;
   unsigned long long excl = 0;
   int64_t q = (int64_t)k - 1;  // nearest predecessor not yet consumed
   for (;;) {
@@ -132,8 +136,15 @@ __device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* 
     q -= take;
     if (!wait && first_pre < 32) break;
   }
-  if (lane == 0) *st = kLbPre | (excl + agg);
+  if (finish && lane == 0) *(volatile unsigned long long*)(status + k) = kLbPre | (excl + agg);
   return excl;
+}
+
+// Both at once (one whole warp): publish, then resolve and finish.
+__device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* status, uint32_t k,
+                                                            uint32_t agg) {
+  if ((threadIdx.x & 31) == 0) tile_publish(status, k, agg);
+  return tile_resolve(status, k, agg, true);
 }
 
 // Host driver.  `part` must hold >= kMaxScanBlocks+1 elements.
