@@ -73,7 +73,7 @@ typedef enum pgpu_order { PGPU_GRLEX = 0, PGPU_LEX = 1 } pgpu_order;
 
 typedef enum pgpu_path {
   PGPU_PATH_AUTO = 0,
-  PGPU_PATH_DENSE = 1,    /* sumset bytemap + per-interval private accumulators    */
+  PGPU_PATH_DENSE = 1,    /* sumset bitmap + per-interval private accumulators     */
   PGPU_PATH_SORT = 2,     /* expand / LSD radix sort / run-length reduce            */
   PGPU_PATH_BUCKET = 3,   /* pairs written once into key-range buckets of <= 2048,
                              each grouped and folded by one CTA in shared memory

@@ -3,14 +3,15 @@
 //
 // The paper's two steps (Alg. 1, PAPER.md; reference parmul.py:64-109):
 //
-//   symbolic  D1 k_symbolic   every pair's compact key marks one byte of a
-//                             sumset bytemap (idempotent byte stores: no
-//                             atomics, order-free).  Replaces the exponent
-//                             sort/merge of heap_merge/tree_merge
-//                             (merge.py:42-62, 113-131): the result exponent
-//                             set is exactly the marked keys, ascending.
-//             D2 k_words      bytemap -> bit words + exclusive rank prefix
-//                             (device scan) + the ascending output key list.
+//   symbolic  D0 k_head_scan  runs of consecutive keys in each operand
+//             D1 k_symbolic   the sumset bitmap as a union of run-pair
+//                             intervals (each key of the window set once,
+//                             order-free).  Replaces the exponent sort/merge
+//                             of heap_merge/tree_merge (merge.py:42-62,
+//                             113-131): the result exponent set is exactly the
+//                             set bits, ascending.
+//             D2 device_scan  bit words -> exclusive rank prefix + the
+//                             ascending output key list.
 //   numeric   D4 k_numeric    one CTA per (row block, segment of consecutive
 //                             intervals).  Interval = D consecutive output
 //                             terms.  Each row keeps a cursor, so its run in
@@ -42,240 +43,95 @@
 namespace pgpu {
 
 // ---- D1 ---------------------------------------------------------------------
-// Tiles of trows x kSymCols pairs (trows = kSymRows unless the product is too
-// small to fill the GPU with such tiles).  A tile is cut into sub-tiles whose key
-// window fits kSymWin bytes: column segments of span < kSymWin/2, then row
-// segments filling the rest (a single row or column has span 0, so every
-// sub-tile fits; the operands are sorted, so segment ends are found by binary
-// search).  A sub-tile marks a shared-memory bytemap over its window
-// (deduplicating the ~16x repeated keys of dense operands) and ORs the marked
-// words into the global bytemap.  Marks are idempotent byte writes of 1: no
-// atomics on per-pair data, independent of order.
-#ifndef PGPU_SYM_UNROLL
-#define PGPU_SYM_UNROLL 4
-#endif
-constexpr int kSymUnroll = PGPU_SYM_UNROLL;
-#ifndef PGPU_SYM_ROWS
-#define PGPU_SYM_ROWS 256
-#endif
-constexpr int kSymRows = PGPU_SYM_ROWS;
-constexpr int kSymCols = 256;
-#ifndef PGPU_SYM_WIN
-#define PGPU_SYM_WIN 49152
-#endif
-constexpr uint32_t kSymWin = PGPU_SYM_WIN;
-constexpr int kSymMaxRowTiles = 512;  // row tiles listed in shared memory (else all tiles visited)
-
-#ifndef PGPU_SYM_SWZ
-#define PGPU_SYM_SWZ 1
-#endif
-// Window slot of window offset o.  Dense keys cluster in the low half of each
-// 64-key block of the lowest fields, so offsets 128 apart share banks; flipping
-// bit 5 by bit 7 moves every other pair of blocks to the unused banks.  The map
-// is an involution inside each aligned 64-byte block.
-__device__ __forceinline__ uint32_t sym_slot(uint32_t o) {
-  PGPU_ASSERT(o < kSymWin);
-  return PGPU_SYM_SWZ ? o ^ ((o >> 2) & 32u) : o;
-}
-
-// largest e in (from, to] with s[e-1] - s[from] <= lim (s ascending)
+// Compact keys of dense operands come in runs of consecutive values (the last
+// field counting up: each Fateman n=30 operand has 5,456 runs of ~8.5 terms),
+// and the keys of (a-run p) x (b-run q) are exactly the interval
+// [first_p + first_q, last_p + last_q].  The sumset is the union of those
+// intervals: 29.8M for F30 instead of 2.15e9 pair keys (operands without runs
+// degrade to one interval per pair).  One CTA per window of ww*32 keys of
+// [R0, R1): the a-runs that can reach the window (binary search), for each
+// the b-runs whose interval meets it (binary search), the clipped interval's
+// bits set in shared memory (atomicOr on its partial end words, plain stores
+// of all-ones words: idempotent, order-free), then the window's words written
+// once to the global bitmap (one owner per word: no atomics, no memset).
 template <typename KT>
-__device__ __forceinline__ uint32_t sym_seg_end(const KT* s, uint32_t from, uint32_t to, uint64_t lim) {
-  const uint64_t k0 = s[from];
-  uint32_t lo = from + 1, hi = to;
+__device__ __forceinline__ uint32_t lower_bound_key(const KT* __restrict__ s, uint32_t n, uint64_t v) {
+  uint32_t lo = 0, hi = n;  // first i with s[i] >= v
   while (lo < hi) {
-    const uint32_t mid = (lo + hi + 1) >> 1;
-    if ((uint64_t)s[mid - 1] - k0 <= lim) lo = mid;
-    else hi = mid - 1;
+    const uint32_t mid = (lo + hi) >> 1;
+    if ((uint64_t)__ldg(s + mid) < v) lo = mid + 1; else hi = mid;
   }
   return lo;
 }
 
+__device__ __forceinline__ void sym_mark(uint32_t* wb, uint32_t s, uint32_t e) {  // bits [s, e), s < e
+  const uint32_t ws = s >> 5, we = (e - 1) >> 5;
+  const uint32_t ms = ~0u << (s & 31), me = ~0u >> (31 - ((e - 1) & 31));
+  if (ws == we) {
+    atomicOr(wb + ws, ms & me);
+    return;
+  }
+  atomicOr(wb + ws, ms);
+  for (uint32_t w = ws + 1; w < we; ++w) wb[w] = ~0u;
+  atomicOr(wb + we, me);
+}
+
+// Lanes take consecutive a-runs (similar keys: similar b-run ranges, little
+// divergence).  (Measured on F30: contiguous a-run shares per thread with
+// galloping bounds, or a block-scanned even split of the intervals, were
+// 1.2-1.4x slower.)
+constexpr int kSymThreads = 256;
+
 template <typename KT>
-__global__ void __launch_bounds__(256)
-k_symbolic(const KT* __restrict__ ak, const KT* __restrict__ bk, const uint32_t* __restrict__ rlo,
-           const uint32_t* __restrict__ rhi, uint32_t na, uint32_t nb, uint64_t R0,
-           uint8_t* __restrict__ bytemap, uint32_t trows) {  // trows <= kSymRows, multiple of 4
-  extern __shared__ __align__(16) uint8_t win[];  // kSymWin bytes
-  __shared__ KT sb[kSymCols];
-  __shared__ __align__(16) KT sa[kSymRows];
-  __shared__ uint32_t slo[kSymRows], shi[kSymRows];
-  __shared__ uint32_t tpre[kSymMaxRowTiles + 1];  // nonempty tiles before row tile rt
-  __shared__ uint16_t tclo[kSymMaxRowTiles];      // first nonempty column tile of row tile rt
-  __shared__ uint32_t tsh[33];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  const uint32_t ntr = (na + trows - 1) / trows, ntc = (nb + kSymCols - 1) / kSymCols;
-  uint64_t ntiles = (uint64_t)ntr * ntc;
-  // List only the tiles that meet the key range: a row tile [r0, r1) meets
-  // columns [rlo[r1-1], rhi[r0]) (row windows shrink leftwards with i).  A
-  // product restricted to a narrow range (one rank of the multi-GPU split)
-  // would otherwise visit every tile of the full pair matrix.
-  const bool listed = ntr <= (uint32_t)kSymMaxRowTiles && ntc <= 65536u;
-  if (listed) {
-    constexpr int C = (kSymMaxRowTiles + 255) / 256;
-    uint32_t cnt[C], sum = 0;
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const uint32_t rt = threadIdx.x * C + c;
-      cnt[c] = 0;
-      if (rt < ntr) {
-        const uint32_t r0 = rt * trows, r1 = min(r0 + trows, na);
-        const uint32_t lo = rlo[r1 - 1], hi = rhi[r0];
-        if (hi > lo) {
-          cnt[c] = (hi - 1) / kSymCols - lo / kSymCols + 1;
-          tclo[rt] = (uint16_t)(lo / kSymCols);
-        }
-      }
-      sum += cnt[c];
+__global__ void __launch_bounds__(kSymThreads)
+k_symbolic(const KT* __restrict__ af, const KT* __restrict__ al, const uint32_t* __restrict__ nra_p,
+           const KT* __restrict__ bf, const KT* __restrict__ bl, const uint32_t* __restrict__ nrb_p,
+           uint64_t R0, uint64_t R1, uint32_t ww, uint32_t* __restrict__ bits) {
+  extern __shared__ uint32_t wb[];  // ww words
+  const uint64_t K0 = R0 + (uint64_t)blockIdx.x * ww * 32;
+  if (K0 >= R1) return;
+  const uint64_t K1 = K0 + (uint64_t)ww * 32 < R1 ? K0 + (uint64_t)ww * 32 : R1;
+  for (uint32_t q = threadIdx.x; q < ww; q += blockDim.x) wb[q] = 0;
+  const uint32_t nra = *nra_p, nrb = *nrb_p;
+  const uint64_t bmin = bf[0], bmax = bl[nrb - 1];
+  // a-runs that can reach the window: last + bmax >= K0 and first + bmin < K1
+  const uint32_t p0 = lower_bound_key(al, nra, K0 > bmax ? K0 - bmax : 0);
+  const uint32_t p1 = lower_bound_key(af, nra, K1 > bmin ? K1 - bmin : 0);
+  __syncthreads();
+  for (uint32_t p = p0 + threadIdx.x; p < p1; p += blockDim.x) {
+    const uint64_t a0 = af[p], a1 = al[p];
+    // b-runs meeting the window with this a-run: last_q >= K0 - a1, first_q < K1 - a0
+    const uint32_t q0 = lower_bound_key(bl, nrb, K0 > a1 ? K0 - a1 : 0);
+    const uint32_t q1 = lower_bound_key(bf, nrb, K1 > a0 ? K1 - a0 : 0);
+    for (uint32_t q = q0; q < q1; ++q) {
+      const uint64_t klo = max(a0 + (uint64_t)__ldg(bf + q), K0);
+      const uint64_t khi = min(a1 + (uint64_t)__ldg(bl + q) + 1, K1);
+      if (klo < khi) sym_mark(wb, (uint32_t)(klo - K0), (uint32_t)(khi - K0));
     }
-    uint32_t tot;
-    uint32_t ex = block_excl_scan(sum, tsh, &tot);
-#pragma unroll
-    for (int c = 0; c < C; ++c) {
-      const uint32_t rt = threadIdx.x * C + c;
-      if (rt < ntr) tpre[rt] = ex;
-      ex += cnt[c];
-    }
-    if (threadIdx.x == 0) tpre[ntr] = tot;
-    __syncthreads();
-    ntiles = tot;
   }
-  for (uint64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-    uint32_t tr, tc;
-    if (listed) {  // row tile: the last rt with tpre[rt] <= tile
-      uint32_t lo = 0, hi = ntr - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (tpre[mid] <= (uint32_t)tile) lo = mid; else hi = mid - 1;
-      }
-      tr = lo;
-      tc = tclo[tr] + ((uint32_t)tile - tpre[tr]);
-    } else {
-      tr = (uint32_t)(tile % ntr);
-      tc = (uint32_t)(tile / ntr);
-    }
-    const uint32_t r0 = tr * trows, r1 = min(r0 + trows, na);
-    const uint32_t c0 = tc * kSymCols, c1 = min(c0 + kSymCols, nb);
-    // rows' column ranges shrink leftwards with i: the tile is empty unless
-    // [rlo[r1-1], rhi[r0]) meets [c0, c1)
-    if (rhi[r0] <= c0 || rlo[r1 - 1] >= c1) continue;
-    for (uint32_t c = c0 + threadIdx.x; c < c1; c += blockDim.x) sb[c - c0] = bk[c];
-    for (uint32_t i = r0 + threadIdx.x; i < r1; i += blockDim.x) {
-      sa[i - r0] = ak[i];
-      slo[i - r0] = rlo[i];
-      shi[i - r0] = rhi[i];
-    }
-    __syncthreads();
-    for (uint32_t cs = 0; cs < c1 - c0;) {
-      const uint32_t ce = sym_seg_end(sb, cs, c1 - c0, kSymWin / 2 - 1);
-      const uint64_t bspan = (uint64_t)sb[ce - 1] - (uint64_t)sb[cs];
-      for (uint32_t rs = 0; rs < r1 - r0;) {
-        const uint32_t re = sym_seg_end(sa, rs, r1 - r0, kSymWin - 128 - bspan);
-        // window aligned to 16 keys (relative to R0) so the flush can OR whole
-        // words; marked keys are >= R0 (rows' column ranges), so clip there
-        const uint64_t kmin = max((uint64_t)sa[rs] + (uint64_t)sb[cs], R0);
-        const uint64_t wlo = R0 + ((kmin - R0) & ~15ull);
-        // bytes in use: the span rounded up to whole 64-byte swizzle blocks
-        const uint32_t wn = ((uint32_t)((uint64_t)sa[re - 1] + (uint64_t)sb[ce - 1] - wlo) + 64u) & ~63u;
-        const uint32_t gc0 = c0 + cs, gc1 = c0 + ce;
-        // rows of the sub-tile meeting its columns (rlo, rhi non-increasing in the row)
-        if (shi[rs] > gc0 && slo[re - 1] < gc1) {
-          for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x)
-            reinterpret_cast<uint4*>(win)[q] = make_uint4(0, 0, 0, 0);
-          __syncthreads();
-          if (slo[rs] <= gc0 && shi[re - 1] >= gc1) {
-            // every row spans every column: thread t owns column cs+t for all
-            // rows, so a mark is one broadcast shared load, an add and a byte store
-            if (threadIdx.x < ce - cs) {
-              const uint32_t boff = (uint32_t)((uint64_t)sb[cs + threadIdx.x] - wlo);
-              uint32_t i = rs;
-              if constexpr (sizeof(KT) == 4) {
-                // four rows' keys per broadcast LDS.128
-                for (; i < re && (i & 3); ++i) win[sym_slot((uint32_t)sa[i] + boff)] = 1;
-#pragma unroll 2
-                for (; i + 4 <= re; i += 4) {
-                  const uint4 k = *reinterpret_cast<const uint4*>(&sa[i]);
-                  win[sym_slot(k.x + boff)] = 1;
-                  win[sym_slot(k.y + boff)] = 1;
-                  win[sym_slot(k.z + boff)] = 1;
-                  win[sym_slot(k.w + boff)] = 1;
-                }
-              }
-#pragma unroll 8
-              for (; i < re; ++i) win[sym_slot((uint32_t)sa[i] + boff)] = 1;
-            }
-          } else {
-            const uint32_t b0 = (uint32_t)sb[0];
-            for (uint32_t i = rs + w; i < re; i += nw) {
-              const uint32_t lo = max(slo[i], gc0), hi = min(shi[i], gc1);
-              const uint32_t ao = (uint32_t)((uint64_t)sa[i] + (uint64_t)sb[0] - wlo);
-              const uint32_t aob = ao - b0;  // window offset = aob + bk (mod 2^32; the sum is in range)
-#pragma unroll kSymUnroll
-              for (uint32_t j = lo + lane; j < hi; j += 32) win[sym_slot(aob + (uint32_t)sb[j - c0])] = 1;
-            }
-          }
-          __syncthreads();
-          // OR the marked words into the global bytemap (other tiles set other bytes
-          // of the same words concurrently, so whole-word plain stores are not safe)
-          unsigned int* dst = reinterpret_cast<unsigned int*>(bytemap + (wlo - R0));
-          for (uint32_t q = threadIdx.x; q * 16 < wn; q += blockDim.x) {
-            const uint4 v = reinterpret_cast<const uint4*>(win)[q];
-            const uint32_t lq = sym_slot(16 * q) / 16;  // the chunk's window offset / 16
-            if (v.x) atomicOr(dst + 4 * lq, v.x);
-            if (v.y) atomicOr(dst + 4 * lq + 1, v.y);
-            if (v.z) atomicOr(dst + 4 * lq + 2, v.z);
-            if (v.w) atomicOr(dst + 4 * lq + 3, v.w);
-          }
-          __syncthreads();
-        }
-        rs = re;
-      }
-      cs = ce;
-    }
-    __syncthreads();
-  }
+  __syncthreads();
+  uint32_t* dst = bits + (K0 - R0) / 32;
+  const uint32_t nw = (uint32_t)((K1 - K0 + 31) / 32);
+  for (uint32_t q = threadIdx.x; q < nw; q += blockDim.x) dst[q] = wb[q];
 }
 
 // ---- D2 ---------------------------------------------------------------------
-// word w covers keys [32w, 32w+32) of the span
+// word w covers keys [R0 + 32w, R0 + 32w + 32)
 struct WordGen {
-  const uint8_t* bytemap;
-  uint64_t span;
-  __device__ uint32_t mask(uint64_t w) const {
-    uint64_t k0 = w * 32;
-    uint32_t m = 0;
-    if (k0 + 32 <= span) {
-      const uint4* p = reinterpret_cast<const uint4*>(bytemap + k0);
-      uint4 x = p[0], y = p[1];
-      uint32_t v[8] = {x.x, x.y, x.z, x.w, y.x, y.y, y.z, y.w};
-#pragma unroll
-      for (int q = 0; q < 8; ++q) {
-        uint32_t t = v[q];
-        // byte b of word q -> bit 4q+b
-        uint32_t nib = (t & 0xffu ? 1u : 0u) | (t & 0xff00u ? 2u : 0u) |
-                       (t & 0xff0000u ? 4u : 0u) | (t & 0xff000000u ? 8u : 0u);
-        m |= nib << (4 * q);
-      }
-    } else {
-      for (uint64_t k = k0; k < span; ++k)
-        if (bytemap[k]) m |= 1u << (k - k0);
-    }
-    return m;
-  }
-  __device__ uint32_t operator()(uint64_t w) const { return __popc(mask(w)); }
+  const uint32_t* bits;
+  __device__ uint32_t mask(uint64_t w) const { return bits[w]; }
+  __device__ uint32_t operator()(uint64_t w) const { return __popc(bits[w]); }
 };
 
 template <typename OKT>
 struct WordOut {
   WordGen gen;
-  uint32_t* bits;
   uint32_t* prefix;
   OKT* okey;
   uint64_t R0;
   uint64_t span_cap;  // key span (checked build: marks stay inside it)
   __device__ void operator()(uint64_t w, uint32_t ex, uint32_t v) const {
     uint32_t m = gen.mask(w);
-    bits[w] = m;
     prefix[w] = ex;
     uint32_t r = ex;
     while (m) {

@@ -147,6 +147,87 @@ __device__ __forceinline__ unsigned long long tile_lookback(unsigned long long* 
   return tile_resolve(status, k, agg, true);
 }
 
+// ---- run heads (single pass) --------------------------------------------
+// Runs of a sorted key array: equal keys (CONSEC = false: the sort path's
+// segments) or consecutive keys k, k+1, k+2, ... (CONSEC = true: the dense
+// path's operand runs).  One read of the keys: tiles of kHsTile keys are
+// claimed in order (ticket), each thread flags the heads among its kHsIpt
+// consecutive keys (16-byte loads), the block scans the flag counts, and warp
+// 0 chains the tile totals by decoupled look-back.  Head r writes
+// starts[r] = i and, when given, first[r] = keys[i] and last[r - 1] =
+// keys[i - 1].  The last tile appends starts[nseg] = n (and last[nseg - 1])
+// and stores nseg to *nseg_out.  status[] (ntiles words) and *ticket are
+// zeroed before the launch.
+constexpr int kHsThreads = 256;
+constexpr int kHsIpt = 16;
+constexpr int kHsTile = kHsThreads * kHsIpt;
+
+template <typename KT, bool CONSEC>
+__global__ void __launch_bounds__(kHsThreads)
+k_head_scan(const KT* __restrict__ keys, uint64_t n, uint32_t* __restrict__ starts,
+            unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket,
+            uint32_t* __restrict__ nseg_out, KT* __restrict__ first = nullptr, KT* __restrict__ last = nullptr) {
+  __shared__ uint32_t sh[33];
+  __shared__ uint32_t s_tile;
+  __shared__ unsigned long long s_excl;
+  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t i0 = (uint64_t)tile * kHsTile + (uint64_t)threadIdx.x * kHsIpt;
+  static_assert(sizeof(KT) * kHsIpt % 16 == 0, "whole 16-byte words per thread");
+  constexpr int W = (int)(sizeof(KT) * kHsIpt / 16);
+  union {
+    uint4 w[W];
+    KT k[kHsIpt];
+  } u;
+  KT prev = 0;  // key i0 - 1
+  uint32_t m = 0;  // bit j: key i0+j is a head
+  auto head = [](KT c, KT p) { return CONSEC ? c != (KT)(p + 1) : c != p; };
+  if (i0 + kHsIpt <= n) {
+    const uint4* src = reinterpret_cast<const uint4*>(keys + i0);
+#pragma unroll
+    for (int j = 0; j < W; ++j) u.w[j] = __ldg(src + j);
+    prev = i0 ? keys[i0 - 1] : (KT)0;
+    KT p = prev;
+#pragma unroll
+    for (int j = 0; j < kHsIpt; ++j) {
+      m |= (i0 + j == 0 || head(u.k[j], p) ? 1u : 0u) << j;
+      p = u.k[j];
+    }
+  } else if (i0 < n) {
+    prev = i0 ? keys[i0 - 1] : (KT)0;
+    KT p = prev;
+    for (int j = 0; j < kHsIpt && i0 + j < n; ++j) {
+      u.k[j] = keys[i0 + j];
+      m |= (i0 + j == 0 || head(u.k[j], p) ? 1u : 0u) << j;
+      p = u.k[j];
+    }
+  }
+  uint32_t tot;
+  uint32_t ex = block_excl_scan((uint32_t)__popc(m), sh, &tot);
+  if (threadIdx.x < 32) {
+    const unsigned long long e = tile_lookback(status, tile, tot);
+    if (threadIdx.x == 0) s_excl = e;
+  }
+  __syncthreads();
+  ex += (uint32_t)s_excl;
+  while (m) {
+    const int j = __ffs(m) - 1;
+    m &= m - 1;
+    starts[ex] = (uint32_t)(i0 + j);
+    if (first) first[ex] = u.k[j];
+    if (last && ex > 0) last[ex - 1] = j ? u.k[j - 1] : prev;
+    ++ex;
+  }
+  const uint64_t ntiles = (n + kHsTile - 1) / kHsTile;
+  if (threadIdx.x == 0 && tile == ntiles - 1) {
+    const uint32_t nseg = (uint32_t)s_excl + tot;
+    starts[nseg] = (uint32_t)n;
+    if (last) last[nseg - 1] = keys[n - 1];
+    *nseg_out = nseg;
+  }
+}
+
 // Host driver.  `part` must hold >= kMaxScanBlocks+1 elements.
 // Returns the number of kernel launches (3).  The total lands in part[*g_out].
 template <typename T, typename Gen, typename Out>

@@ -601,75 +601,8 @@ k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restr
   }
 }
 
-// ---- K3: run-length heads -> segment starts (single pass) -----------------
-// One read of the sorted keys: tiles of kHsTile keys are claimed in order
-// (ticket), each thread flags the heads among its kHsIpt consecutive keys
-// (16-byte loads), the block scans the flag counts, and warp 0 chains the
-// tile totals by decoupled look-back (scan.cuh).  Heads write their index at
-// their rank: starts[r] = i.  The last tile appends starts[nseg] = n and
-// stores nseg to *nseg_out.  status[] (ntiles words) and *ticket are zeroed
-// before the launch.
-constexpr int kHsThreads = 256;
-constexpr int kHsIpt = 16;
-constexpr int kHsTile = kHsThreads * kHsIpt;
-
-template <typename KT>
-__global__ void __launch_bounds__(kHsThreads)
-k_head_scan(const KT* __restrict__ keys, uint64_t n, uint32_t* __restrict__ starts,
-            unsigned long long* __restrict__ status, uint32_t* __restrict__ ticket,
-            uint32_t* __restrict__ nseg_out) {
-  __shared__ uint32_t sh[33];
-  __shared__ uint32_t s_tile;
-  __shared__ unsigned long long s_excl;
-  if (threadIdx.x == 0) s_tile = atomicAdd(ticket, 1u);
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t i0 = (uint64_t)tile * kHsTile + (uint64_t)threadIdx.x * kHsIpt;
-  static_assert(sizeof(KT) * kHsIpt % 16 == 0, "whole 16-byte words per thread");
-  constexpr int W = (int)(sizeof(KT) * kHsIpt / 16);
-  union {
-    uint4 w[W];
-    KT k[kHsIpt];
-  } u;
-  uint32_t m = 0;  // bit j: key i0+j is a head
-  if (i0 + kHsIpt <= n) {
-    const uint4* src = reinterpret_cast<const uint4*>(keys + i0);
-#pragma unroll
-    for (int j = 0; j < W; ++j) u.w[j] = __ldg(src + j);
-    KT prev = i0 ? keys[i0 - 1] : ~u.k[0];
-#pragma unroll
-    for (int j = 0; j < kHsIpt; ++j) {
-      m |= (u.k[j] != prev ? 1u : 0u) << j;
-      prev = u.k[j];
-    }
-  } else if (i0 < n) {
-    KT prev = i0 ? keys[i0 - 1] : ~keys[i0];
-    for (int j = 0; j < kHsIpt && i0 + j < n; ++j) {
-      const KT c = keys[i0 + j];
-      m |= (c != prev ? 1u : 0u) << j;
-      prev = c;
-    }
-  }
-  uint32_t tot;
-  uint32_t ex = block_excl_scan((uint32_t)__popc(m), sh, &tot);
-  if (threadIdx.x < 32) {
-    const unsigned long long e = tile_lookback(status, tile, tot);
-    if (threadIdx.x == 0) s_excl = e;
-  }
-  __syncthreads();
-  ex += (uint32_t)s_excl;
-  while (m) {
-    const int j = __ffs(m) - 1;
-    m &= m - 1;
-    starts[ex++] = (uint32_t)(i0 + j);
-  }
-  const uint64_t ntiles = (n + kHsTile - 1) / kHsTile;
-  if (threadIdx.x == 0 && tile == ntiles - 1) {
-    const uint32_t nseg = (uint32_t)s_excl + tot;
-    starts[nseg] = (uint32_t)n;
-    *nseg_out = nseg;
-  }
-}
+// ---- K3: run-length heads -> segment starts ---------------------------------
+// k_head_scan<KT, false> (scan.cuh): one pass over the sorted keys.
 
 // ---- K4: segment reduce (one owner per output term) -------------------------
 // G lanes own one segment (G = 1, 2, ..., 32, picked from the mean segment

@@ -45,7 +45,7 @@ def test_golden_cases_dense_when_applicable(case):
     name, a, b, split, want = case
     try:
         got = mul(a, b, MulConfig(path="dense"), split=None if split is None else SplitSet(split))
-    except Exception as exc:  # key span too wide for a bytemap: the dense path refuses loudly
+    except Exception as exc:  # key span too wide for the sumset bitmap: the dense path refuses loudly
         assert "dense path" in str(exc)
         return
     _check(got, want)
