@@ -33,5 +33,7 @@ if [ -z "$NO_FULL" ]; then
   full k_rs_count mp25 int 40
   full k_gen_j mp25 int 12
   full k_seg_reduce_int_j mp25 int 12
+  full k_head_scan mp12 int 1
+  full k_head_scan mp25 int 40
 fi
 du -sh $OUT; ls -la $OUT | tail -40
