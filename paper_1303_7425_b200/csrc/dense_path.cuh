@@ -418,7 +418,6 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
     }
     __syncthreads();
     uint32_t* my = acc + w * DP;
-    uint8_t* myc = cbyte + w * DP;
     // one step: kUnroll columns per lane of row (akr, a0/ad) from cursor c; invalid
     // lanes add into their private pad slot so the step has no divergent branch
     const uint64_t span_t = Khi - 1 - Klo;
@@ -505,45 +504,46 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
           if (cy) cbyte[w * DP + slot[u]] += 1;
         }
         return nv;
-      }
+      } else {
 #pragma unroll
-      for (int u = 0; u < kUnroll; ++u) {
-        const uint32_t j = okk[u] ? c + lane + 32 * u : 0u;
-        if constexpr (MODE == 0) {
-          double* d = reinterpret_cast<double*>(acc) + w * DP + slot[u];
-          const double bv = okk[u] ? __ldg(reinterpret_cast<const double*>(A.bc) + j) : 0.0;
-          *d = __dadd_rn(*d, __dmul_rn(ad, bv));
-        } else if constexpr (MODE == 1) {
-          const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
-          const uint64_t lo = a0 * b0;
-          uint32_t p[NW];
-          const uint64_t hi = __umul64hi(a0, b0);
-          const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
+        for (int u = 0; u < kUnroll; ++u) {
+          const uint32_t j = okk[u] ? c + lane + 32 * u : 0u;
+          if constexpr (MODE == 0) {
+            double* d = reinterpret_cast<double*>(acc) + w * DP + slot[u];
+            const double bv = okk[u] ? __ldg(reinterpret_cast<const double*>(A.bc) + j) : 0.0;
+            *d = __dadd_rn(*d, __dmul_rn(ad, bv));
+          } else if constexpr (MODE == 1) {
+            const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
+            const uint64_t lo = a0 * b0;
+            uint32_t p[NW];
+            const uint64_t hi = __umul64hi(a0, b0);
+            const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
 #pragma unroll
-          for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : 0u;
-          add_words<NW, STRIDE>(my + slot[u], p);
-        } else if constexpr (MODE == 2) {
-          const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
-          const uint64_t lo = a0 * b0;
-          const uint64_t hi = (uint64_t)__mul64hi((long long)a0, (long long)b0);
-          const uint32_t ext = (uint32_t)((int64_t)hi >> 63);
-          const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
-          uint32_t p[NW];
+            for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : 0u;
+            add_words<NW, STRIDE>(my + slot[u], p);
+          } else if constexpr (MODE == 2) {
+            const uint64_t b0 = okk[u] ? (uint64_t)__ldg(reinterpret_cast<const long long*>(A.bc) + j) : 0ull;
+            const uint64_t lo = a0 * b0;
+            const uint64_t hi = (uint64_t)__mul64hi((long long)a0, (long long)b0);
+            const uint32_t ext = (uint32_t)((int64_t)hi >> 63);
+            const uint32_t w4[4] = {(uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32)};
+            uint32_t p[NW];
 #pragma unroll
-          for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : ext;
-          add_words<NW, STRIDE>(my + slot[u], p);
-        } else {
-          ICoef ca = load_icoef<2>(A.ac, ri);
-          ICoef cb = load_icoef<2>(A.bc, j);
-          if (!okk[u]) cb.x0 = cb.x1 = cb.x2 = 0;
-          Limbs<3> pr = imul<3, 2>(ca, cb);
-          uint32_t p[NW];
+            for (int k = 0; k < NW; ++k) p[k] = k < 4 ? w4[k] : ext;
+            add_words<NW, STRIDE>(my + slot[u], p);
+          } else {
+            ICoef ca = load_icoef<2>(A.ac, ri);
+            ICoef cb = load_icoef<2>(A.bc, j);
+            if (!okk[u]) cb.x0 = cb.x1 = cb.x2 = 0;
+            Limbs<3> pr = imul<3, 2>(ca, cb);
+            uint32_t p[NW];
 #pragma unroll
-          for (int k = 0; k < NW; ++k) p[k] = (uint32_t)(pr.w[k >> 1] >> (32 * (k & 1)));
-          add_words<NW, STRIDE>(my + slot[u], p);
+            for (int k = 0; k < NW; ++k) p[k] = (uint32_t)(pr.w[k >> 1] >> (32 * (k & 1)));
+            add_words<NW, STRIDE>(my + slot[u], p);
+          }
         }
+        return nv;
       }
-      return nv;
     };
     auto rows = [&](auto tbl_mode) {
       // integers: warps claim 32-row groups dynamically (one shared counter per

@@ -685,7 +685,6 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
     return fail(PGPU_EINVAL, "operand exponents are not strictly ascending packed words");
   // exponent fit (core.py:365-385): field sums must stay within the caps
   for (int f = 0; f < P.nf; ++f) {
-    int w = lay->width[f];
     uint64_t cap = P.mask[f];
     if (f == 0) cap -= 1;  // grlex degree ceiling / lex top-field ceiling reserved
     uint64_t s = hs.fmax[0][f] + hs.fmax[1][f];
@@ -694,7 +693,6 @@ int build_problem(Ctx& ctx, const pgpu_layout* lay, const pgpu_options* opt, Pro
                   (P.order == 0 && f == 0) ? "total degree" : "exponent", f,
                   (unsigned long long)s, (unsigned long long)cap);
     }
-    (void)w;
   }
   // exact coefficient width.  |c_k| <= sum over its pairs |a_i||b_j|, which is
   // <= min(na,nb)*max|a|*max|b| and <= min(sum|a|*max|b|, max|a|*sum|b|).

@@ -205,7 +205,6 @@ template <typename KT>
 __global__ void __launch_bounds__(kRsThreads)
 k_rs_hist_all(const KT* __restrict__ keys, uint64_t n, int npass, unsigned int* __restrict__ ghist) {
   __shared__ uint32_t h[kRsMaxPasses][kRsDigits];
-  const int lane = threadIdx.x & 31;
   for (int k = threadIdx.x; k < kRsMaxPasses * kRsDigits; k += blockDim.x) (&h[0][0])[k] = 0;
   __syncthreads();
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
