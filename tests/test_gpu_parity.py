@@ -490,3 +490,40 @@ def test_golden_cases_sort_path_column_records(case, monkeypatch):
     name, a, b, split, want = case
     got = mul(a, b, MulConfig(path="sort", float_ordered=True), split=None if split is None else SplitSet(split))
     _check(got, want)
+
+
+@pytest.mark.parametrize("shape", ["one_run", "no_runs", "mixed"])
+def test_dense_symbolic_run_intervals_vs_oracle(shape, rng):
+    """The dense path's sumset is a union of (a-run x b-run) key intervals
+    (dense_path.cuh D1).  Operands made of one long run (runs far wider than a
+    window), of isolated keys (one interval per pair) and of mixed run
+    lengths, whole and restricted to consecutive packed ranges, against the
+    oracle (exact ints)."""
+    from oracle import oracle as O
+    from paper_1303_7425_b200.core import Polynomial as P
+    from paper_1303_7425_b200.parmul import limbs_to_ints
+    lay = default_layout(("x", "y"))
+
+    def exps(n, top):
+        if shape == "one_run":
+            return [(0, e) for e in range(n)]
+        if shape == "no_runs":
+            return [(0, 2 * e) for e in range(n)]
+        pool = sorted(rng.sample(range(top), n))
+        return [(e // 64, e % 64) for e in pool]
+
+    def poly(n, top):
+        return P(lay, [(rng.randint(-10 ** 9, 10 ** 9), e) for e in exps(n, top)], int)
+
+    a, b = poly(3000, 9000), poly(2500, 9000)
+    want = O.mul(a, b)
+    A, B = Operand.from_poly(a), Operand.from_poly(b)
+    got = native_mul(A, B, lay, path="dense")
+    assert got.path == "dense"
+    assert got.exps.tolist() == want.exps
+    assert limbs_to_ints(got.coef, got.nl) == want.coeffs
+    bounds = select_grid(a, b, GridParams(7)).bounds
+    cuts = [0] + bounds[1:-1:2] + [(1 << 64) - 1]
+    parts = [native_mul(A, B, lay, lo=lo, hi=hi, path="dense") for lo, hi in zip(cuts, cuts[1:])]
+    assert np.array_equal(np.concatenate([p.exps for p in parts]), got.exps)
+    assert np.array_equal(np.concatenate([p.coef for p in parts]), got.coef)
