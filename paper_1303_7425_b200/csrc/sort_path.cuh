@@ -666,6 +666,9 @@ k_seg_reduce_f64(const KT* __restrict__ keys, const uint64_t* __restrict__ vals,
 
 // K4 on j-records: the segment's key gives every pair's a-term through the
 // key/coefficient hash (a_i = key + KL - b_j), then the same folds as above.
+#ifndef PGPU_SEG_UNROLL
+#define PGPU_SEG_UNROLL 1  // MP n=25 reduce 224 ms at 2, 238 at 4, 213 at 1; MP n=12 equal
+#endif
 template <typename RT, int NL, int CK, int G>
 __global__ void __launch_bounds__(256)
 k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ vals,
@@ -680,15 +683,22 @@ k_seg_reduce_int_j(const RT* __restrict__ keys, const uint32_t* __restrict__ val
   Limbs<NL> acc;
   limbs_zero(acc);
   uint32_t p = p0 + g;
-  // two pairs per iteration: both gathers of each are issued before either is used
-  for (; p + G < p1; p += 2 * G) {
-    const uint32_t j0 = vals[p], j1 = vals[p + G];
-    const KCSlot b0 = brec[j0], b1 = brec[j1];
-    const KCSlot a0 = ahash.find(key - b0.key), a1 = ahash.find(key - b1.key);
-    limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a0), kc_icoef<CK>(b0)));
-    limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a1), kc_icoef<CK>(b1)));
+  // PGPU_SEG_UNROLL pairs per iteration: every gather of each is issued before
+  // any is used (three dependent loads per pair: column, b record, a slot)
+  constexpr int U = PGPU_SEG_UNROLL;
+  for (; p + (U - 1) * G < p1; p += U * G) {
+    uint32_t j[U];
+    KCSlot b[U], a[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) j[u] = vals[p + u * G];
+#pragma unroll
+    for (int u = 0; u < U; ++u) b[u] = brec[j[u]];
+#pragma unroll
+    for (int u = 0; u < U; ++u) a[u] = ahash.find(key - b[u].key);
+#pragma unroll
+    for (int u = 0; u < U; ++u) limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a[u]), kc_icoef<CK>(b[u])));
   }
-  if (p < p1) {
+  for (; p < p1; p += G) {
     const KCSlot b = brec[vals[p]];
     const KCSlot a = ahash.find(key - b.key);
     limbs_add(acc, imul<NL, CK>(kc_icoef<CK>(a), kc_icoef<CK>(b)));
