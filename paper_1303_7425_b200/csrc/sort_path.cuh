@@ -382,7 +382,7 @@ k_rs_onesweep(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __rest
 // The onesweep's decoupled look-back walks every predecessor tile still in
 // flight (~600 on the GPU): on MP n=25 batches its spinning was ~90% of the
 // pass's instructions and the pass ran at ~2 TB/s.  Here a pass is
-//   RS1 k_rs_count    per super-tile (kRsSuper consecutive tiles) digit counts,
+//   RS1 k_rs_count    per super-tile (sup consecutive tiles) digit counts,
 //                     digit-major cnt[d][st]; reads the keys only
 //   RS2 k_rs_colscan  per digit: exclusive scan over the super-tiles (in
 //                     place) and the digit total
@@ -404,7 +404,8 @@ constexpr uint64_t kRsSuperItems = (uint64_t)kRsSuper * kRsTile;
 
 template <typename KT>
 __global__ void __launch_bounds__(kRsThreads)
-k_rs_count(const KT* __restrict__ keys, uint64_t n, int shift, uint32_t nst, uint32_t* __restrict__ cnt) {
+k_rs_count(const KT* __restrict__ keys, uint64_t n, int shift, uint32_t nst, uint32_t sup,
+           uint32_t* __restrict__ cnt) {
   // one histogram per warp, plain shared-memory atomics: after the first
   // pass the digits of a warp's 32 keys rarely collide, and a warp-level
   // match per key made the pass MIO-bound (match + atomic per key)
@@ -413,8 +414,8 @@ k_rs_count(const KT* __restrict__ keys, uint64_t n, int shift, uint32_t nst, uin
   const int w = threadIdx.x >> 5;
   for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&h[0][0])[k] = 0;
   __syncthreads();
-  const uint64_t b0 = (uint64_t)st * kRsSuperItems;
-  const uint64_t b1 = b0 + kRsSuperItems < n ? b0 + kRsSuperItems : n;
+  const uint64_t b0 = (uint64_t)st * sup * kRsTile;
+  const uint64_t b1 = b0 + (uint64_t)sup * kRsTile < n ? b0 + (uint64_t)sup * kRsTile : n;
   // 16-byte loads (V keys per thread per round; b0 is a multiple of V and the
   // arrays are 256-byte aligned)
   constexpr int V = 16 / sizeof(KT);
@@ -482,8 +483,8 @@ __global__ void __launch_bounds__(1024) k_rs_colscan(uint32_t* __restrict__ cnt,
 template <typename KT, typename VT = uint64_t>
 __global__ void __launch_bounds__(kRsThreads, PGPU_RS_SCAT_MINB)
 k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restrict__ kout,
-             VT* __restrict__ vout, uint64_t n, int shift, uint32_t nst, const uint32_t* __restrict__ cnt,
-             const uint32_t* __restrict__ tot) {
+             VT* __restrict__ vout, uint64_t n, int shift, uint32_t nst, uint32_t sup,
+             const uint32_t* __restrict__ cnt, const uint32_t* __restrict__ tot) {
   extern __shared__ __align__(16) uint8_t rs_smem[];
   VT* sval = reinterpret_cast<VT*>(rs_smem);                         // [kRsTile]
   KT* skey = reinterpret_cast<KT*>(rs_smem + sizeof(VT) * kRsTile);  // [kRsTile]
@@ -501,7 +502,7 @@ k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restr
     const uint32_t ex = block_excl_scan(tot[d], shs, &t);
     run[d] = (unsigned long long)ex + cnt[(uint64_t)d * nst + st];
   }
-  const uint64_t s0 = (uint64_t)st * kRsSuperItems;
+  const uint64_t s0 = (uint64_t)st * sup * kRsTile;
   // The next tile is copied into a shared-memory buffer with cp.async while
   // this one is ranked and scattered (no registers held for it, so three
   // CTAs fit an SM).  16-byte chunks; a partial last tile is zero-filled.
@@ -527,7 +528,7 @@ k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restr
   if (s0 < n) prefetch(s0);
   KT key[kRsIpt];
   VT val[kRsIpt];
-  for (int tl = 0; tl < kRsSuper; ++tl) {
+  for (uint32_t tl = 0; tl < sup; ++tl) {
     const uint64_t t0 = s0 + (uint64_t)tl * kRsTile;
     if (t0 >= n) break;
     const uint64_t end = t0 + kRsTile < n ? t0 + kRsTile : n;
@@ -541,7 +542,7 @@ k_rs_scatter(const KT* __restrict__ kin, const VT* __restrict__ vin, KT* __restr
     }
     for (int k = threadIdx.x; k < kRsWarps * kRsDigits; k += blockDim.x) (&wcnt[0][0])[k] = 0;
     __syncthreads();  // buffer read by all: refill it with the next tile
-    if (tl + 1 < kRsSuper && t0 + kRsTile < n) prefetch(t0 + kRsTile);
+    if (tl + 1 < sup && t0 + kRsTile < n) prefetch(t0 + kRsTile);
     uint32_t rank[kRsIpt];
     unsigned dig[kRsIpt];
 #pragma unroll
