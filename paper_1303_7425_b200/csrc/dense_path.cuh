@@ -701,8 +701,14 @@ __device__ __forceinline__ void numeric_unit(const NumArgs& A, const uint32_t un
 #ifndef PGPU_PERSISTENT
 #define PGPU_PERSISTENT 1
 #endif
+// Two CTAs per SM are resident either way (their accumulators fill shared
+// memory), so the register budget is 64 per thread, not the 40 ptxas picks
+// for a bare 512-thread bound (which spilled the f64 and 3-4 plane modes).
+#ifndef PGPU_NUMERIC_MINB
+#define PGPU_NUMERIC_MINB 2
+#endif
 template <typename KT, int NW, int MODE, int CB>
-__global__ void __launch_bounds__(kNumThreads)
+__global__ void __launch_bounds__(kNumThreads, PGPU_NUMERIC_MINB)
 k_numeric(NumArgs A) {
 #if PGPU_PERSISTENT
   __shared__ uint32_t unit_s;
